@@ -1,0 +1,153 @@
+/*
+ * flashoptim_b200.h -- C ABI of the B200 (sm_100a) FlashOptim step library
+ * (libflashoptim_b200.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Every device pointer is a
+ * CUDA global-memory address; `stream` is a cudaStream_t passed as void*.
+ * Each entry point names the reference function it replaces
+ * (/root/reference/pkg/src/flashopt/<file>:<line>).  The reference API is a
+ * set of pure NumPy functions; the C ABI is the in-place, stream-ordered
+ * device form of the same contract:
+ *
+ *   reference                                  C ABI
+ *   optim.adamw_step(state, grad, hp)  :406    fo_adamw_step / fo_step_mt(FO_OPT_ADAMW)
+ *   optim.sgd_step(state, grad, hp)    :385    fo_sgd_step   / fo_step_mt(FO_OPT_SGD)
+ *   optim.lion_step(state, grad, hp)   :436    fo_lion_step  / fo_step_mt(FO_OPT_LION)
+ *   optim.STEP_FUNCTIONS               :459    fo_step_mt's `optimizer` argument
+ *   optim.init_flash_state             :341    fo_split + zeroed codes/scales
+ *   formats.split                      :232    fo_split
+ *   formats.reconstruct                :248    fo_reconstruct
+ *   quantize.quantize_momentum         :109    fo_quantize_momentum
+ *   quantize.dequantize_momentum       :125    fo_dequantize_momentum
+ *   quantize.quantize_variance         :134    fo_quantize_variance
+ *   quantize.dequantize_variance       :152    fo_dequantize_variance
+ *
+ * Error behaviour.  The reference raises ValueError before producing any
+ * output.  Device kernels cannot raise: each launch ORs FO_ERR_* bits into
+ * the caller-owned device word `d_err` (may be NULL to skip reporting) and
+ * the buffers are updated regardless.  fo_error_message() maps a mask to the
+ * message the reference would have raised first.  Host-side argument errors
+ * (bad sizes, unsupported layouts) are returned synchronously as FO_E*.
+ */
+#ifndef FLASHOPTIM_B200_H
+#define FLASHOPTIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FO_ABI_VERSION 1
+
+/* Return codes (>0 values are cudaError_t). */
+#define FO_OK 0
+#define FO_EINVAL (-1)       /* bad argument (null pointer, size, unknown enum) */
+#define FO_EUNSUPPORTED (-2) /* layout the library does not implement */
+#define FO_ETOOMANY (-3)     /* hyper-parameter table larger than FO_MAX_HPARAMS */
+
+/* Device error bits, one per reference ValueError class and buffer. */
+#define FO_ERR_GRAD_NONFINITE 0x01u  /* optim.py:381 "gradient-nonfinite" */
+#define FO_ERR_RHO_INVALID 0x02u     /* formats.py:271 "invalid-correction-code" */
+#define FO_ERR_SPLIT_NONFINITE 0x04u /* formats.py:243 "split-nonfinite" */
+#define FO_ERR_M_NONFINITE 0x08u     /* quantize.py:69 "quantize-nonfinite" (momentum) */
+#define FO_ERR_M_OVERFLOW 0x10u      /* quantize.py:85,92 "scale-overflow" (momentum) */
+#define FO_ERR_V_NONFINITE 0x20u     /* quantize.py:69 "quantize-nonfinite" (variance) */
+#define FO_ERR_V_NEGATIVE 0x40u      /* quantize.py:144 "negative-variance" */
+#define FO_ERR_V_OVERFLOW 0x80u      /* quantize.py:85,92 "scale-overflow" (variance) */
+
+/* Optimizer tags = FLOP v1 header tags (checkpoint.py:54). */
+#define FO_OPT_SGD 0
+#define FO_OPT_ADAMW 1
+#define FO_OPT_LION 2
+
+/* Gradient element types.  The reference upcasts any grad to f32
+ * (optim.py:377); bf16 is the training-time layout, f32 the exact one. */
+#define FO_GRAD_BF16 0
+#define FO_GRAD_F32 1
+
+/* Variance storage schemes (optim.py:362-373). */
+#define FO_VAR_COMPANDED 0
+#define FO_VAR_LINEAR 1
+
+#define FO_MAX_HPARAMS 16
+
+/* Per-step float32 scalars, formed on the host exactly as the reference
+ * forms them: Python floats rounded once to f32 (NEP 50), 1-beta and the
+ * bias corrections 1-beta**t evaluated in float64 then rounded once
+ * (optim.py:410-411, 418-419, 445-446).  Fill with fo_make_hparams(). */
+typedef struct fo_hparams {
+  float lr, wd, eps;
+  float b1, omb1; /* beta1 and f32(1-beta1)          (AdamW, Lion) */
+  float b2, omb2; /* beta2 and f32(1-beta2)          (AdamW, Lion) */
+  float mu;       /* SGD momentum                    (SGD)         */
+  float bc1, bc2; /* f32(1-beta1**t), f32(1-beta2**t) (AdamW)      */
+  float rbc1, rbc2; /* RN(1/bc1), RN(1/bc2) (f32 division; used for exact Markstein quotients) */
+} fo_hparams;
+
+/* One flat parameter tensor's state (FLOP v1 record names,
+ * checkpoint.py:111-123).  All element pointers cover `n` elements; scale
+ * pointers cover ceil(n / group_size) fp16 values.  v_* are NULL for
+ * SGD/Lion.  `hp_index` selects the fo_hparams entry (param group). */
+typedef struct fo_tensor {
+  void *lp;        /* "weights.lp"      bf16 bits, u16[n], in/out  */
+  void *rho;       /* "weights.rho"     i8[n] (or i16[n]), in/out  */
+  void *m_codes;   /* "momentum.codes"  i8[n], in/out              */
+  void *m_scales;  /* "momentum.scales" f16[ceil(n/G)], in/out     */
+  void *v_codes;   /* "variance.codes"  u8[n], in/out (AdamW)      */
+  void *v_scales;  /* "variance.scales" f16[ceil(n/G)], in/out     */
+  const void *grad;/* bf16[n] or f32[n], read only                 */
+  int64_t n;
+  int32_t hp_index;
+  int32_t reserved;
+} fo_tensor;
+
+/* Library / device queries. */
+uint32_t fo_abi_version(void);
+const char *fo_status_string(int status);
+/* Message of the reference ValueError that `mask` corresponds to for
+ * `optimizer` (first in the reference's program order), or "" if mask==0.
+ * Precedence: optim.py:406-433 (AdamW), :385-403 (SGD), :436-456 (Lion). */
+const char *fo_error_message(uint32_t mask, int optimizer);
+
+/* Host helper: the reference's per-step f32 scalars (optim.py:408-424). */
+void fo_make_hparams(int optimizer, double lr, double beta1, double beta2, double eps, double weight_decay,
+                     double momentum, int64_t t, fo_hparams *out);
+
+/* Multi-tensor fused step: the whole parameter list in as few launches as
+ * possible (one per FO_MT_MAX_TENSORS tensors), stream-ordered on `stream`.
+ * Replaces a Python loop of STEP_FUNCTIONS[opt](state, grad, hp) calls
+ * (training.py:219-226).  `tensors` and `hparams` are HOST arrays, read
+ * before return.  rho_bits 8|16, group_size >= 1 (32 is the fused fast
+ * path), variance_scheme FO_VAR_*. */
+int fo_step_mt(int optimizer, const fo_tensor *tensors, int32_t n_tensors, const fo_hparams *hparams,
+               int32_t n_hparams, int grad_dtype, int rho_bits, int32_t group_size, int variance_scheme,
+               uint32_t *d_err, void *stream);
+
+/* Single-tensor steps, in place (optim.py:406, :385, :436). */
+int fo_adamw_step(uint16_t *lp, int8_t *rho, int8_t *m_codes, uint16_t *m_scales, uint8_t *v_codes,
+                  uint16_t *v_scales, const void *grad, int grad_dtype, int64_t n, const fo_hparams *hp,
+                  uint32_t *d_err, void *stream);
+int fo_sgd_step(uint16_t *lp, int8_t *rho, int8_t *m_codes, uint16_t *m_scales, const void *grad, int grad_dtype,
+                int64_t n, const fo_hparams *hp, uint32_t *d_err, void *stream);
+int fo_lion_step(uint16_t *lp, int8_t *rho, int8_t *m_codes, uint16_t *m_scales, const void *grad, int grad_dtype,
+                 int64_t n, const fo_hparams *hp, uint32_t *d_err, void *stream);
+
+/* Codecs (formats.py:232-276, quantize.py:109-158), device buffers. */
+int fo_split(const float *theta, int64_t n, uint16_t *lp, void *rho, int rho_bits, uint32_t *d_err, void *stream);
+int fo_reconstruct(const uint16_t *lp, const void *rho, int rho_bits, int64_t n, float *out, uint32_t *d_err,
+                   void *stream);
+int fo_quantize_momentum(const float *m, int64_t n, int32_t group_size, int8_t *codes, uint16_t *scales,
+                         uint32_t *d_err, void *stream);
+int fo_dequantize_momentum(const int8_t *codes, const uint16_t *scales, int64_t n, int32_t group_size, float *out,
+                           void *stream);
+int fo_quantize_variance(const float *v, int64_t n, int32_t group_size, uint8_t *codes, uint16_t *scales,
+                         uint32_t *d_err, void *stream);
+int fo_dequantize_variance(const uint8_t *codes, const uint16_t *scales, int64_t n, int32_t group_size, float *out,
+                           void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHOPTIM_B200_H */

@@ -1,0 +1,156 @@
+// fo_api.cu -- the extern "C" boundary (include/flashoptim_b200.h).
+// Argument validation happens here, synchronously, before anything is
+// enqueued; everything else is stream-ordered on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "fo_internal.h"
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+const char* kMsg[8] = {
+    "gradient-nonfinite: gradient contains NaN/Inf",                 // optim.py:381
+    "invalid-correction-code: asymmetric minimum is forbidden",      // formats.py:271
+    "split-nonfinite: cannot split NaN/Inf master weights",          // formats.py:243
+    "quantize-nonfinite: state buffer contains NaN/Inf",             // quantize.py:69
+    "scale-overflow: group absmax exceeds FP16 range",               // quantize.py:85
+    "quantize-nonfinite: state buffer contains NaN/Inf",             // quantize.py:69
+    "negative-variance: variance entries must be >= 0",              // quantize.py:144
+    "scale-overflow: group absmax exceeds FP16 range",               // quantize.py:85
+};
+
+int check_opt(int opt) { return (opt == FO_OPT_SGD || opt == FO_OPT_ADAMW || opt == FO_OPT_LION) ? 0 : FO_EINVAL; }
+
+}  // namespace
+
+extern "C" {
+
+uint32_t fo_abi_version(void) { return FO_ABI_VERSION; }
+
+const char* fo_status_string(int status) {
+  switch (status) {
+    case FO_OK: return "ok";
+    case FO_EINVAL: return "invalid argument";
+    case FO_EUNSUPPORTED: return "unsupported layout";
+    case FO_ETOOMANY: return "too many hyper-parameter sets";
+    default: return status > 0 ? cudaGetErrorString((cudaError_t)status) : "unknown status";
+  }
+}
+
+const char* fo_error_message(uint32_t mask, int optimizer) {
+  // Program order of each reference step: the first failing stage raises.
+  static const uint32_t adamw[] = {FO_ERR_GRAD_NONFINITE, FO_ERR_RHO_INVALID, FO_ERR_SPLIT_NONFINITE,
+                                   FO_ERR_M_NONFINITE,    FO_ERR_M_OVERFLOW,  FO_ERR_V_NONFINITE,
+                                   FO_ERR_V_NEGATIVE,     FO_ERR_V_OVERFLOW};
+  static const uint32_t sgd[] = {FO_ERR_GRAD_NONFINITE, FO_ERR_M_NONFINITE, FO_ERR_M_OVERFLOW, FO_ERR_RHO_INVALID,
+                                 FO_ERR_SPLIT_NONFINITE};
+  static const uint32_t lion[] = {FO_ERR_GRAD_NONFINITE, FO_ERR_RHO_INVALID, FO_ERR_SPLIT_NONFINITE,
+                                  FO_ERR_M_NONFINITE, FO_ERR_M_OVERFLOW};
+  const uint32_t* order = adamw;
+  int count = 8;
+  if (optimizer == FO_OPT_SGD) order = sgd, count = 5;
+  if (optimizer == FO_OPT_LION) order = lion, count = 5;
+  for (int i = 0; i < count; ++i)
+    if (mask & order[i]) return kMsg[__builtin_ctz(order[i])];
+  for (int b = 0; b < 8; ++b)
+    if (mask & (1u << b)) return kMsg[b];
+  return "";
+}
+
+void fo_make_hparams(int optimizer, double lr, double beta1, double beta2, double eps, double weight_decay,
+                     double momentum, int64_t t, fo_hparams* out) {
+  (void)optimizer;
+  out->lr = (float)lr;
+  out->wd = (float)weight_decay;
+  out->eps = (float)eps;
+  out->b1 = (float)beta1;
+  out->omb1 = (float)(1.0 - beta1);
+  out->b2 = (float)beta2;
+  out->omb2 = (float)(1.0 - beta2);
+  out->mu = (float)momentum;
+  out->bc1 = (float)(1.0 - std::pow(beta1, (double)t));  // optim.py:410
+  out->bc2 = (float)(1.0 - std::pow(beta2, (double)t));  // optim.py:411
+  volatile float one = 1.0f;                                // f32 division: RN(1/bc)
+  out->rbc1 = one / out->bc1;
+  out->rbc2 = one / out->bc2;
+}
+
+int fo_step_mt(int optimizer, const fo_tensor* tensors, int32_t n_tensors, const fo_hparams* hparams,
+               int32_t n_hparams, int grad_dtype, int rho_bits, int32_t group_size, int variance_scheme,
+               uint32_t* d_err, void* stream) {
+  if (check_opt(optimizer) || n_tensors < 0 || (n_tensors && !tensors) || !hparams || n_hparams < 1)
+    return FO_EINVAL;
+  if (n_hparams > FO_MAX_HPARAMS) return FO_ETOOMANY;
+  if (grad_dtype != FO_GRAD_BF16 && grad_dtype != FO_GRAD_F32) return FO_EINVAL;
+  if (rho_bits != 8 && rho_bits != 16) return FO_EINVAL;
+  if (group_size < 1) return FO_EINVAL;
+  if (variance_scheme != FO_VAR_COMPANDED && variance_scheme != FO_VAR_LINEAR) return FO_EINVAL;
+  for (int32_t i = 0; i < n_tensors; ++i) {
+    const fo_tensor& t = tensors[i];
+    if (t.n < 0 || t.hp_index < 0 || t.hp_index >= n_hparams) return FO_EINVAL;
+    if (t.n == 0) continue;
+    if (!t.lp || !t.rho || !t.m_codes || !t.m_scales || !t.grad) return FO_EINVAL;
+    if (optimizer == FO_OPT_ADAMW && (!t.v_codes || !t.v_scales)) return FO_EINVAL;
+  }
+  return fo::step_mt(optimizer, tensors, n_tensors, hparams, n_hparams, grad_dtype, rho_bits, group_size,
+                     variance_scheme, d_err, as_stream(stream));
+}
+
+int fo_adamw_step(uint16_t* lp, int8_t* rho, int8_t* m_codes, uint16_t* m_scales, uint8_t* v_codes,
+                  uint16_t* v_scales, const void* grad, int grad_dtype, int64_t n, const fo_hparams* hp,
+                  uint32_t* d_err, void* stream) {
+  fo_tensor t{lp, rho, m_codes, m_scales, v_codes, v_scales, grad, n, 0, 0};
+  return fo_step_mt(FO_OPT_ADAMW, &t, 1, hp, 1, grad_dtype, 8, 32, FO_VAR_COMPANDED, d_err, stream);
+}
+
+int fo_sgd_step(uint16_t* lp, int8_t* rho, int8_t* m_codes, uint16_t* m_scales, const void* grad, int grad_dtype,
+                int64_t n, const fo_hparams* hp, uint32_t* d_err, void* stream) {
+  fo_tensor t{lp, rho, m_codes, m_scales, nullptr, nullptr, grad, n, 0, 0};
+  return fo_step_mt(FO_OPT_SGD, &t, 1, hp, 1, grad_dtype, 8, 32, FO_VAR_COMPANDED, d_err, stream);
+}
+
+int fo_lion_step(uint16_t* lp, int8_t* rho, int8_t* m_codes, uint16_t* m_scales, const void* grad, int grad_dtype,
+                 int64_t n, const fo_hparams* hp, uint32_t* d_err, void* stream) {
+  fo_tensor t{lp, rho, m_codes, m_scales, nullptr, nullptr, grad, n, 0, 0};
+  return fo_step_mt(FO_OPT_LION, &t, 1, hp, 1, grad_dtype, 8, 32, FO_VAR_COMPANDED, d_err, stream);
+}
+
+int fo_split(const float* theta, int64_t n, uint16_t* lp, void* rho, int rho_bits, uint32_t* d_err, void* stream) {
+  if (n < 0 || (n && (!theta || !lp || !rho)) || (rho_bits != 8 && rho_bits != 16)) return FO_EINVAL;
+  return fo::split(theta, n, lp, rho, rho_bits, d_err, as_stream(stream));
+}
+
+int fo_reconstruct(const uint16_t* lp, const void* rho, int rho_bits, int64_t n, float* out, uint32_t* d_err,
+                   void* stream) {
+  if (n < 0 || (n && (!lp || !rho || !out)) || (rho_bits != 8 && rho_bits != 16)) return FO_EINVAL;
+  return fo::reconstruct(lp, rho, rho_bits, n, out, d_err, as_stream(stream));
+}
+
+int fo_quantize_momentum(const float* m, int64_t n, int32_t group_size, int8_t* codes, uint16_t* scales,
+                         uint32_t* d_err, void* stream) {
+  if (n < 0 || group_size < 1 || (n && (!m || !codes || !scales))) return FO_EINVAL;
+  return fo::quantize(false, m, n, group_size, codes, scales, d_err, as_stream(stream));
+}
+
+int fo_dequantize_momentum(const int8_t* codes, const uint16_t* scales, int64_t n, int32_t group_size, float* out,
+                           void* stream) {
+  if (n < 0 || group_size < 1 || (n && (!codes || !scales || !out))) return FO_EINVAL;
+  return fo::dequantize(false, codes, scales, n, group_size, out, as_stream(stream));
+}
+
+int fo_quantize_variance(const float* v, int64_t n, int32_t group_size, uint8_t* codes, uint16_t* scales,
+                         uint32_t* d_err, void* stream) {
+  if (n < 0 || group_size < 1 || (n && (!v || !codes || !scales))) return FO_EINVAL;
+  return fo::quantize(true, v, n, group_size, codes, scales, d_err, as_stream(stream));
+}
+
+int fo_dequantize_variance(const uint8_t* codes, const uint16_t* scales, int64_t n, int32_t group_size, float* out,
+                           void* stream) {
+  if (n < 0 || group_size < 1 || (n && (!codes || !scales || !out))) return FO_EINVAL;
+  return fo::dequantize(true, codes, scales, n, group_size, out, as_stream(stream));
+}
+
+}  // extern "C"

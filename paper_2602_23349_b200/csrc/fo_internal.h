@@ -1,0 +1,27 @@
+// fo_internal.h -- shared declarations between the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+#include <vector>
+
+#include "flashoptim_b200.h"
+
+// Max tensors per fused launch: the whole table travels as one
+// __grid_constant__ kernel parameter block (< 32 KB, CUDA >= 12.1).
+#define FO_MT_MAX_TENSORS 384
+
+namespace fo {
+
+int step_mt(int opt, const fo_tensor* ts, int32_t nt, const fo_hparams* hps, int32_t nhp, int grad_dtype,
+            int rho_bits, int32_t G, int var_scheme, uint32_t* d_err, cudaStream_t s);
+int split(const float* theta, int64_t n, uint16_t* lp, void* rho, int rho_bits, uint32_t* d_err, cudaStream_t s);
+int reconstruct(const uint16_t* lp, const void* rho, int rho_bits, int64_t n, float* out, uint32_t* d_err,
+                cudaStream_t s);
+int quantize(bool variance, const float* x, int64_t n, int64_t G, void* codes, uint16_t* scales, uint32_t* d_err,
+             cudaStream_t s);
+int dequantize(bool variance, const void* codes, const uint16_t* scales, int64_t n, int64_t G, float* out,
+               cudaStream_t s);
+
+}  // namespace fo
