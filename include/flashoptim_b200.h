@@ -147,6 +147,15 @@ int fo_quantize_variance(const float *v, int64_t n, int32_t group_size, uint8_t 
 int fo_dequantize_variance(const uint8_t *codes, const uint16_t *scales, int64_t n, int32_t group_size, float *out,
                            void *stream);
 
+/* Device self-check of the fast exact primitives against the IEEE
+ * intrinsics (no reference counterpart; test support).  mode 0: sqrt over
+ * f32 bit patterns [begin, begin+count); 1: reciprocal of every fp16 value;
+ * 2/3/4: hash-sampled quotients (per-element, per-group-scale and
+ * bias-correction divisors).  d_out[0] += mismatches, d_out[1] = min failing
+ * index (initialise to 0 and UINT64_MAX); mode 5 writes raw sqrt results to
+ * d_out[2..] (debug). */
+int fo_selftest(int mode, uint64_t begin, uint64_t count, uint64_t *d_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

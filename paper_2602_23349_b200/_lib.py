@@ -13,7 +13,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libflashoptim_b200.so")
+LIB_PATH = os.environ.get("FO_LIB_PATH") or os.path.join(_HERE, "libflashoptim_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 FO_OK = 0
@@ -72,6 +72,7 @@ SIGNATURES = {
     "fo_dequantize_momentum": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
     "fo_quantize_variance": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _P]),
     "fo_dequantize_variance": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
+    "fo_selftest": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _P, _P]),
 }
 
 _lib = None

@@ -153,4 +153,9 @@ int fo_dequantize_variance(const uint8_t* codes, const uint16_t* scales, int64_t
   return fo::dequantize(true, codes, scales, n, group_size, out, as_stream(stream));
 }
 
+int fo_selftest(int mode, uint64_t begin, uint64_t count, uint64_t* d_out, void* stream) {
+  if (!d_out) return FO_EINVAL;
+  return fo::selftest(mode, begin, count, reinterpret_cast<unsigned long long*>(d_out), as_stream(stream));
+}
+
 }  // extern "C"
