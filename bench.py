@@ -230,6 +230,8 @@ def run_ours(args) -> None:
     grads = [grads_flat[o:o + n] for o, n in zip(fl.offsets, fl.sizes)]
     plan = StepPlan(opt, fl.states)
     plan.set_grads(grads)
+    for st in fl.states:  # the random state stands for a step t0 of a training run
+        st.t = args.t0
     hp = HP_TYPES[opt](**hparams_for(args.config, opt))
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -292,7 +294,8 @@ def run_ours(args) -> None:
                        "hbm_gbs_equiv": value * bpp,
                        "l2": "working set >> 126 MB L2 (no flush needed)" if n_local * bpp > 1e9
                        else "L2-resident working set",
-                       "parallelism": f"zero1-shard{world}" if world > 1 else "single"},
+                       "parallelism": f"zero1-shard{world}" if world > 1 else "single",
+                       "step_t": args.t0},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
@@ -315,6 +318,8 @@ def main():
     ap.add_argument("--config", default="llama31_8b", choices=["llama31_8b", "gpt2_medium", "resnet50"])
     ap.add_argument("--optimizer", default="adamw", choices=["adamw", "sgd", "lion"])
     ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--t0", type=int, default=1000,
+                    help="step counter of the synthetic state (1000: steady state, f32 bias corrections == 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

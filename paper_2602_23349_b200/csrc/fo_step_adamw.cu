@@ -1,0 +1,13 @@
+// fo_step_adamw.cu -- instantiates the fused adamw step (fo_step_impl.cuh).
+#include "fo_step_impl.cuh"
+
+namespace fo {
+
+int step_adamw(const fo_tensor* ts, int32_t nt, const fo_hparams* hps, int32_t nhp, int grad_dtype, int rho_bits,
+             int32_t G, int var_scheme, uint32_t* d_err, cudaStream_t s) {
+  return grad_dtype == FO_GRAD_BF16
+             ? step_mt_typed<FO_OPT_ADAMW, __nv_bfloat16>(ts, nt, hps, nhp, rho_bits, G, var_scheme, d_err, s)
+             : step_mt_typed<FO_OPT_ADAMW, float>(ts, nt, hps, nhp, rho_bits, G, var_scheme, d_err, s);
+}
+
+}  // namespace fo
