@@ -125,6 +125,18 @@ int fo_step_mt(int optimizer, const fo_tensor *tensors, int32_t n_tensors, const
                int32_t n_hparams, int grad_dtype, int rho_bits, int32_t group_size, int variance_scheme,
                uint32_t *d_err, void *stream);
 
+/* Host-resident state (the reference's calling convention: NumPy arrays in
+ * host memory, optim.py:385-459).  Every pointer in `tensors` is a HOST
+ * pointer (pinned for full PCIe bandwidth; pageable works).  The list is cut
+ * into group-aligned pieces that stream through `chunk_elems`-element device
+ * slots (0 = 64M): H2D copy, fused step, D2H copy on three rotating slots
+ * and streams.  Synchronous; the error mask is written to *h_err. */
+int fo_step_host(int optimizer, const fo_tensor *tensors, int32_t n_tensors, const fo_hparams *hparams,
+                 int32_t n_hparams, int grad_dtype, int rho_bits, int32_t group_size, int variance_scheme,
+                 int64_t chunk_elems, uint32_t *h_err);
+/* Free the device slots fo_step_host keeps between calls. */
+void fo_host_release(void);
+
 /* Single-tensor steps, in place (optim.py:406, :385, :436). */
 int fo_adamw_step(uint16_t *lp, int8_t *rho, int8_t *m_codes, uint16_t *m_scales, uint8_t *v_codes,
                   uint16_t *v_scales, const void *grad, int grad_dtype, int64_t n, const fo_hparams *hp,

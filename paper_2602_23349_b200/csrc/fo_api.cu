@@ -99,6 +99,28 @@ int fo_step_mt(int optimizer, const fo_tensor* tensors, int32_t n_tensors, const
                      variance_scheme, d_err, as_stream(stream));
 }
 
+int fo_step_host(int optimizer, const fo_tensor* tensors, int32_t n_tensors, const fo_hparams* hparams,
+                 int32_t n_hparams, int grad_dtype, int rho_bits, int32_t group_size, int variance_scheme,
+                 int64_t chunk_elems, uint32_t* h_err) {
+  if (check_opt(optimizer) || n_tensors < 0 || (n_tensors && !tensors) || !hparams || n_hparams < 1)
+    return FO_EINVAL;
+  if (n_hparams > FO_MAX_HPARAMS) return FO_ETOOMANY;
+  if ((grad_dtype != FO_GRAD_BF16 && grad_dtype != FO_GRAD_F32) || (rho_bits != 8 && rho_bits != 16) ||
+      group_size < 1 || (variance_scheme != FO_VAR_COMPANDED && variance_scheme != FO_VAR_LINEAR) || chunk_elems < 0)
+    return FO_EINVAL;
+  for (int32_t i = 0; i < n_tensors; ++i) {
+    const fo_tensor& t = tensors[i];
+    if (t.n < 0 || t.hp_index < 0 || t.hp_index >= n_hparams) return FO_EINVAL;
+    if (t.n == 0) continue;
+    if (!t.lp || !t.rho || !t.m_codes || !t.m_scales || !t.grad) return FO_EINVAL;
+    if (optimizer == FO_OPT_ADAMW && (!t.v_codes || !t.v_scales)) return FO_EINVAL;
+  }
+  return fo::step_host(optimizer, tensors, n_tensors, hparams, n_hparams, grad_dtype, rho_bits, group_size,
+                       variance_scheme, chunk_elems, h_err);
+}
+
+void fo_host_release(void) { fo::host_release(); }
+
 int fo_adamw_step(uint16_t* lp, int8_t* rho, int8_t* m_codes, uint16_t* m_scales, uint8_t* v_codes,
                   uint16_t* v_scales, const void* grad, int grad_dtype, int64_t n, const fo_hparams* hp,
                   uint32_t* d_err, void* stream) {

@@ -21,6 +21,9 @@ int reconstruct(const uint16_t* lp, const void* rho, int rho_bits, int64_t n, fl
                 cudaStream_t s);
 int quantize(bool variance, const float* x, int64_t n, int64_t G, void* codes, uint16_t* scales, uint32_t* d_err,
              cudaStream_t s);
+int step_host(int opt, const fo_tensor* ts, int32_t nt, const fo_hparams* hps, int32_t nhp, int grad_dtype,
+              int rho_bits, int32_t G, int var_scheme, int64_t chunk_elems, uint32_t* h_err);
+void host_release();
 int selftest(int mode, uint64_t begin, uint64_t count, unsigned long long* d_out, cudaStream_t s);
 int dequantize(bool variance, const void* codes, const uint16_t* scales, int64_t n, int64_t G, float* out,
                cudaStream_t s);
