@@ -198,6 +198,55 @@ def init_random_state(fl, grads_flat, seed: int):
             v.copy_(torch.randn(v.numel(), generator=gen, device=dev) * scale)
 
 
+def host_e2e(fl, grads_flat, opt, hp, t0, steps, warmup):
+    """e2e: the same step through the C-ABI host-buffer entry point
+    (fo_step_host): state + gradient in pinned host memory, H2D copy, fused
+    step and D2H copy of the updated state inside the timed region."""
+    import numpy as np
+    import torch
+
+    from paper_2602_23349_b200.host import HostFlashState, pinned_empty, step_host
+
+    t_alloc = time.perf_counter()
+    n_tot, g_tot = fl.total, fl.gtotal
+    host = {}
+    for name, buf, dt in (("lp", fl.lp, np.uint16), ("rho", fl.rho, np.int8), ("mq", fl.m_codes, np.int8),
+                          ("ms", fl.m_scales, np.float16), ("vq", fl.v_codes, np.uint8),
+                          ("vs", fl.v_scales, np.float16), ("g", grads_flat, np.uint16)):
+        if buf is None:
+            host[name] = None
+            continue
+        a = pinned_empty(buf.numel(), dt)
+        torch.from_numpy(a.view({1: np.uint8, 2: np.int16}[a.itemsize])).copy_(
+            buf.view({1: torch.uint8, 2: torch.int16}[buf.element_size()]))
+        host[name] = a
+    states, grads = [], []
+    h2d = d2h = 0
+    for o, go, n in zip(fl.offsets, fl.goffsets, fl.sizes):
+        ng = -(-n // 32)
+        st = HostFlashState(host["lp"][o:o + n], host["rho"][o:o + n], host["mq"][o:o + n],
+                            host["ms"][go:go + ng], None if host["vq"] is None else host["vq"][o:o + n],
+                            None if host["vs"] is None else host["vs"][go:go + ng], t0)
+        states.append(st)
+        grads.append(host["g"][o:o + n])
+        adam = opt == "adamw"
+        h2d += n * (2 + 1 + 1 + (1 if adam else 0) + 2) + ng * 2 * (2 if adam else 1)
+        d2h += n * (2 + 1 + 1 + (1 if adam else 0)) + ng * 2 * (2 if adam else 1)
+    alloc_s = time.perf_counter() - t_alloc
+    for _ in range(warmup):
+        step_host(opt, states, grads, hp, chunk_elems=1 << 26, check=False)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(steps):
+        step_host(opt, states, grads, hp, chunk_elems=1 << 26, check=False)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t) / steps
+    return {"value": sum(fl.sizes) / dt / 1e9, "unit": "Gparams/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3, "steps": steps, "warmup": warmup,
+            "path": "fo_step_host (C ABI), pinned host buffers, 3 x 64M-element device slots",
+            "host_setup_s": round(alloc_s, 1)}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -214,23 +263,21 @@ def run_ours(args) -> None:
     opt = args.optimizer
     shapes = S.CONFIGS[args.config]()
     sizes = [S.numel(s) for _, s in shapes]
-    # ZeRO-1 style sharding for N>1: each rank owns a contiguous, 64-aligned
-    # 1/N slice of every tensor (no collective on the timed data path).
+    # N > 1: ZeRO-1 layout, each rank owns a contiguous 64-aligned 1/N slice
+    # of every tensor (paper_2602_23349_b200/zero.py); the step itself has no
+    # collective, so the timed region is the sharded step on every rank.
     if world > 1:
-        shard_sizes = []
-        for n in sizes:
-            per = -(-n // world)
-            per = -(-per // 64) * 64
-            lo = min(n, rank * per)
-            shard_sizes.append(max(0, min(n, lo + per) - lo))
-        sizes = [s for s in shard_sizes if s > 0]
+        from paper_2602_23349_b200.zero import shard_range
+
+        sizes = [b - a for a, b in (shard_range(n, rank, world) for n in sizes)]
+        sizes = [s for s in sizes if s > 0]
     fl = FlatStates(sizes, opt, dev)
     grads_flat = torch.empty(fl.total, dtype=torch.bfloat16, device=dev)
     init_random_state(fl, grads_flat, 1234 + rank)
     grads = [grads_flat[o:o + n] for o, n in zip(fl.offsets, fl.sizes)]
     plan = StepPlan(opt, fl.states)
     plan.set_grads(grads)
-    for st in fl.states:  # the random state stands for a step t0 of a training run
+    for st in fl.states:  # the random state stands for step t0 of a training run
         st.t = args.t0
     hp = HP_TYPES[opt](**hparams_for(args.config, opt))
     err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -266,7 +313,7 @@ def run_ours(args) -> None:
         dist.barrier()
     clk = clocks.stop()
     total_ms = t0.elapsed_time(t1)
-    kern_ms = sorted(a.elapsed_time(b) for a, b in ev)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
     avg_kern_ms = sum(kern_ms) / len(kern_ms)
     if world > 1:
         tt = torch.tensor([total_ms, avg_kern_ms], device=dev)
@@ -283,27 +330,36 @@ def run_ours(args) -> None:
     peak, peak_kind = peaks()
     bpp = BYTES_PER_PARAM[opt]
     achieved = n_local * bpp / (avg_kern_ms * 1e-3) / 1e9
-    line = None
+    launches_per_step = len(plan.launch_groups()) if hasattr(plan, "launch_groups") else (len(sizes) + 383) // 384
+
+    e2e = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        e2e = host_e2e(fl, grads_flat, opt, hp, args.t0 + args.warmup + args.steps,
+                       steps=min(args.steps, args.e2e_steps), warmup=1)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_sample_run(opt, args.config, args.ref_seconds, len(os.sched_getaffinity(0)))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gparams/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32 math on bf16/i8/u8/f16 storage", "data": "synthetic",
-            "config": {"workload": f"{args.config} Flash{opt} fused step, state resident in HBM",
+            "config": {"workload": f"{args.config} Flash{opt} fused step (state resident in HBM)",
                        "optimizer": opt, "params": n_all, "tensors": len(shapes),
-                       "hbm_gbs_equiv": value * bpp,
-                       "l2": "working set >> 126 MB L2 (no flush needed)" if n_local * bpp > 1e9
+                       "hbm_gbs_equiv": value * bpp, "step_t": args.t0 + 1,
+                       "l2": "working set >> 126 MB L2, no flush needed" if n_local * bpp > 1e9
                        else "L2-resident working set",
-                       "parallelism": f"zero1-shard{world}" if world > 1 else "single",
-                       "step_t": args.t0},
+                       "parallelism": f"zero1-shard{world}" if world > 1 else "single-gpu"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": args.traffic,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                         "bytes_per_param": bpp, "kernel_ms": avg_kern_ms},
-            "clocks": clk, "gpu_launches": args.steps * ((len(sizes) + 383) // 384),
+                         "bytes_per_param": bpp, "kernel_ms": avg_kern_ms,
+                         "kernel": "fo::step_tma_kernel (cuda events on the launch stream)"},
+            "e2e": e2e, "cpu_baseline": cpu,
+            "clocks": clk, "gpu_launches": args.steps * launches_per_step,
             "device_errors": emask,
         }
-    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -318,6 +374,11 @@ def main():
     ap.add_argument("--config", default="llama31_8b", choices=["llama31_8b", "gpt2_medium", "resnet50"])
     ap.add_argument("--optimizer", default="adamw", choices=["adamw", "sgd", "lion"])
     ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch (read+write), from profiles/, reported beside the roofline")
     ap.add_argument("--t0", type=int, default=1000,
                     help="step counter of the synthetic state (1000: steady state, f32 bias corrections == 1)")
     args = ap.parse_args()

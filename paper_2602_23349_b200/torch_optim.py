@@ -1,0 +1,246 @@
+"""torch.optim front end: FlashAdamW, FlashSGD, FlashLion.
+
+Drop-in optimizers over the fused CUDA step.  The reference package has no
+torch classes (its API is optim.py's pure functions over FlashState); this is
+the torch.optim surface the build promises (BASELINE.json north_star), mapped
+one to one onto the reference state:
+
+    param.data (bf16)           <-> FlashState.weights.lp_values  "weights.lp"
+    state["weights.rho"]        <-> FlashState.weights.corrections
+    state["momentum.codes"]     <-> FlashState.momentum.codes
+    state["momentum.scales"]    <-> FlashState.momentum.scales (fp16)
+    state["variance.codes"]     <-> FlashState.variance.codes  (AdamW)
+    state["variance.scales"]    <-> FlashState.variance.scales (AdamW)
+    state["step"]               <-> FlashState.t
+
+(the keys are the FLOP v1 record names, checkpoint.py:111-123).  Defaults are
+the reference's (optim.py:47-94): AdamW betas (0.9, 0.999), eps 1e-8,
+weight_decay 0 (note: torch.optim.AdamW defaults to 0.01); SGD momentum 0.9;
+Lion betas (0.9, 0.99).  Hyper-parameters are validated with the reference's
+rules and messages.
+
+fp32 parameters are split once into bf16 + int8 correction
+(init_flash_state, optim.py:143-161): `param.data` becomes the bf16 tensor,
+so the model trains on bf16 weights while the optimizer keeps 24-bit master
+weights.  bf16 parameters start with zero corrections.
+
+All parameters of a param group go to the GPU in one fused launch per step
+(fo_step_mt); errors are checked after the step (one device-to-host read)
+unless `check_errors=False`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Iterable
+
+import torch
+
+from . import _lib
+from ._errors import DeviceErrors, raise_for_mask, stream_handle
+from .formats import INT8_CORRECTION, SplitTensor, split
+from .optim import AdamHyperParams, FlashState, LionHyperParams, SgdHyperParams
+from .quantize import GroupSpec, QuantizedState
+
+__all__ = ["FlashAdamW", "FlashSGD", "FlashLion", "FlashOptimizer"]
+
+RECORDS = ("weights.rho", "momentum.codes", "momentum.scales", "variance.codes", "variance.scales")
+
+
+class FlashOptimizer(torch.optim.Optimizer):
+    """Shared machinery; subclasses define OPT and hp(group)."""
+
+    OPT = ""
+
+    def __init__(self, params, defaults: dict, *, check_errors: bool = True, group_size: int = 32):
+        self.check_errors = check_errors
+        self.spec = GroupSpec(group_size)
+        super().__init__(params, defaults)
+        for group in self.param_groups:
+            self.hp(group)  # validate with the reference's rules
+            for p in group["params"]:
+                self._init_state(p)
+        self._errors: DeviceErrors | None = None
+        self._plans: dict = {}
+
+    # -- state -----------------------------------------------------------------
+    def _init_state(self, p: torch.Tensor) -> None:
+        st = self.state[p]
+        if "weights.rho" in st:
+            return
+        if not p.is_cuda:
+            raise ValueError("FlashOptim B200 optimizers need CUDA parameters (no CPU path)")
+        n, dev = p.numel(), p.device
+        with torch.no_grad():
+            if p.dtype == torch.float32:
+                lp, rho = split(p.detach().reshape(-1), INT8_CORRECTION)  # init_flash_state
+                p.data = lp.view(p.shape)
+                st["weights.rho"] = rho.view(p.shape)
+            elif p.dtype == torch.bfloat16:
+                st["weights.rho"] = torch.zeros(p.shape, dtype=torch.int8, device=dev)
+            else:
+                raise TypeError(f"parameters must be bf16 or fp32, got {p.dtype}")
+        ng = self.spec.num_groups(n)
+        st["momentum.codes"] = torch.zeros(p.shape, dtype=torch.int8, device=dev)
+        st["momentum.scales"] = torch.zeros(ng, dtype=torch.float16, device=dev)
+        if self.OPT == "adamw":
+            st["variance.codes"] = torch.zeros(p.shape, dtype=torch.uint8, device=dev)
+            st["variance.scales"] = torch.zeros(ng, dtype=torch.float16, device=dev)
+        st["step"] = 0
+
+    def flash_state(self, p: torch.Tensor) -> FlashState:
+        """The reference-shaped FlashState view of a parameter's state (shares memory)."""
+        st = self.state[p]
+        w = SplitTensor(p.data.reshape(-1), st["weights.rho"].reshape(-1))
+        m = QuantizedState(st["momentum.codes"].reshape(-1), st["momentum.scales"], self.spec, "momentum")
+        v = None
+        if self.OPT == "adamw":
+            v = QuantizedState(st["variance.codes"].reshape(-1), st["variance.scales"], self.spec, "variance")
+        return FlashState(w, m, v, int(st["step"]))
+
+    def hp(self, group: dict):
+        raise NotImplementedError
+
+    # -- step ------------------------------------------------------------------
+    def _launch(self, params: list, grads: list, group: dict, stream=None, errors: DeviceErrors | None = None):
+        """One fused launch for `params` (all from `group`)."""
+        hp = self.hp(group)
+        tensors, scalars, index, keep = [], [], {}, []
+        gdt = None
+        all_bf16 = all(g.dtype == torch.bfloat16 for g in grads)  # else every grad goes as f32
+        for p, g in zip(params, grads):
+            st = self.state[p]
+            t = int(st["step"]) + 1
+            if t not in index:
+                index[t] = len(scalars)
+                scalars.append(hp.scalars(t))
+            g = (g if all_bf16 else g.float()).contiguous()
+            gdt = g.dtype
+            keep.append(g)  # converted grads stay alive until the launch is stream-ordered
+            adam = self.OPT == "adamw"
+            tensors.append(_lib.fo_tensor(
+                p.data.data_ptr(), st["weights.rho"].data_ptr(), st["momentum.codes"].data_ptr(),
+                st["momentum.scales"].data_ptr(), st["variance.codes"].data_ptr() if adam else None,
+                st["variance.scales"].data_ptr() if adam else None, g.data_ptr(), p.numel(), index[t], 0))
+        if gdt is None:
+            return
+        if len(scalars) > _lib.FO_MAX_HPARAMS:
+            raise ValueError("too many distinct step counters in one param group")
+        arr = (_lib.fo_tensor * len(tensors))(*tensors)
+        hp_arr = (_lib.fo_hparams * len(scalars))(*scalars)
+        dev = params[0].device
+        sh = stream.cuda_stream if stream is not None else stream_handle(dev)
+        errs = errors or self._errors
+        _lib.check(_lib.lib().fo_step_mt(
+            _lib.OPT_TAGS[self.OPT], arr, len(tensors), hp_arr, len(scalars),
+            _lib.FO_GRAD_BF16 if gdt == torch.bfloat16 else _lib.FO_GRAD_F32, 8, self.spec.group_size,
+            _lib.FO_VAR_COMPANDED, errs.ptr if errs is not None else None, sh), "fo_step_mt")
+        if stream is not None:
+            for g in keep:
+                g.record_stream(stream)
+        for p in params:
+            self.state[p]["step"] = int(self.state[p]["step"]) + 1
+
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = None
+        if closure is not None:
+            with torch.enable_grad():
+                loss = closure()
+        dev = None
+        for group in self.param_groups:
+            ps = [p for p in group["params"] if p.grad is not None]
+            if not ps:
+                continue
+            dev = ps[0].device
+            if self._errors is None or self._errors.word.device != dev:
+                self._errors = DeviceErrors(dev)
+            self._launch(ps, [p.grad.reshape(-1) for p in ps], group)
+        if self.check_errors and dev is not None:
+            self.raise_errors()
+        return loss
+
+    def raise_errors(self) -> None:
+        """Raise the reference's ValueError for any error the kernels flagged
+        since the last check (one device-to-host read)."""
+        if self._errors is None:
+            return
+        m = self._errors.mask()
+        if m:
+            self._errors.reset()
+            raise_for_mask(m, self.OPT)
+
+    # -- torch.optim plumbing ----------------------------------------------------
+    # torch.optim.Optimizer.load_state_dict casts floating-point state to the
+    # parameter dtype (bf16), which would round the fp16 scales; they travel
+    # as their int16 bit patterns instead and are restored bit for bit.
+    _SCALES = ("momentum.scales", "variance.scales")
+
+    def state_dict(self) -> dict:
+        sd = super().state_dict()
+        packed = {}
+        for pid, st in sd["state"].items():
+            st = dict(st)
+            for k in self._SCALES:
+                if k in st and st[k].dtype == torch.float16:
+                    st[k] = st[k].view(torch.int16)
+            packed[pid] = st
+        sd["state"] = packed
+        return sd
+
+    def load_state_dict(self, state_dict: dict) -> None:
+        super().load_state_dict(state_dict)
+        for group in self.param_groups:
+            for p in group["params"]:
+                st = self.state[p]
+                for k in self._SCALES:
+                    if k in st:
+                        v = st[k]
+                        st[k] = v.view(torch.float16) if v.dtype == torch.int16 else v.to(torch.float16)
+                if "step" in st:
+                    st["step"] = int(st["step"])
+                if p.dtype == torch.float32:  # a fresh model: the checkpoint holds bf16 weights.lp
+                    p.data = p.data.to(torch.bfloat16)
+
+
+class FlashAdamW(FlashOptimizer):
+    """FlashAdamW (optim.py:208-235): decoupled weight decay, exact-integer bias correction."""
+
+    OPT = "adamw"
+
+    def __init__(self, params: Iterable, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
+                 weight_decay: float = 0.0, **kw):
+        super().__init__(params, dict(lr=lr, betas=tuple(betas), eps=eps, weight_decay=weight_decay), **kw)
+
+    def hp(self, g: dict) -> AdamHyperParams:
+        return AdamHyperParams(lr=float(g["lr"]), beta1=float(g["betas"][0]), beta2=float(g["betas"][1]),
+                               eps=float(g["eps"]), weight_decay=float(g["weight_decay"]))
+
+
+class FlashSGD(FlashOptimizer):
+    """FlashSGD (optim.py:187-205): m <- mu*m + g; theta <- theta - lr*(m + wd*theta)."""
+
+    OPT = "sgd"
+
+    def __init__(self, params: Iterable, lr: float = 1e-2, momentum: float = 0.9, weight_decay: float = 0.0, **kw):
+        super().__init__(params, dict(lr=lr, momentum=momentum, weight_decay=weight_decay), **kw)
+
+    def hp(self, g: dict) -> SgdHyperParams:
+        return SgdHyperParams(lr=float(g["lr"]), momentum=float(g["momentum"]), weight_decay=float(g["weight_decay"]))
+
+
+class FlashLion(FlashOptimizer):
+    """FlashLion (optim.py:238-258)."""
+
+    OPT = "lion"
+
+    def __init__(self, params: Iterable, lr: float = 1e-4, betas=(0.9, 0.99), weight_decay: float = 0.0, **kw):
+        super().__init__(params, dict(lr=lr, betas=tuple(betas), weight_decay=weight_decay), **kw)
+
+    def hp(self, g: dict) -> LionHyperParams:
+        return LionHyperParams(lr=float(g["lr"]), beta1=float(g["betas"][0]), beta2=float(g["betas"][1]),
+                               weight_decay=float(g["weight_decay"]))
+
+
+# ctypes is re-exported for callers that build their own launch tables
+_ = ctypes

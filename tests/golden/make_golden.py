@@ -94,6 +94,16 @@ def main() -> None:
         qm_x=m, qm_codes=qm.codes, qm_scales=qm.scales, qm_deq=Q.dequantize_momentum(qm),
         qv_x=m * m, qv_codes=qv.codes, qv_scales=qv.scales, qv_deq=Q.dequantize_variance(qv),
     )
+    # --- FLOP v1 files written by the reference ------------------------------
+    C = fo.checkpoint
+    rng = np.random.default_rng(5)
+    for opt, n in (("adamw", 1003), ("sgd", 64), ("lion", 33)):
+        st = H.random_state(rng, n, opt)
+        fs = R.to_ref_state(st, int(rng.integers(1, 1 << 40)))
+        C.save_checkpoint(fs, os.path.join(HERE, f"ckpt_{opt}.flop"), optimizer=opt)
+    st = H.random_state(rng, 100, "adamw")
+    st["weights.rho"] = rng.integers(-32767, 32768, 100).astype(np.int16)
+    C.save_checkpoint(R.to_ref_state(st, 9), os.path.join(HERE, "ckpt_adamw_rho16.flop"))
     with open(os.path.join(HERE, "index.json"), "w") as f:
         json.dump(index, f, indent=1, sort_keys=True)
     print("wrote", sorted(os.listdir(HERE)))

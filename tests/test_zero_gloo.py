@@ -1,0 +1,141 @@
+"""CPU, world_size 2 (gloo): the ZeRO-1 layout and collectives.
+
+The sharded optimizer (paper_2602_23349_b200/zero.py) runs with the C oracle
+injected as its step (no GPU here); after several steps every rank's full
+parameters and every shard's state must equal a single-process, unsharded
+oracle run bit for bit.  Gradients are exact under the bf16 reduce-scatter:
+rank 0 contributes g, rank 1 zeros, op=sum."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+SIZES = [1000, 4096 + 7, 33, 70_000, 1]
+STEPS = 3
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _np(t: torch.Tensor) -> np.ndarray:
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).numpy().view(np.uint16)
+    return t.numpy()
+
+
+def _oracle_step_fn(opt, states, grads, hps):
+    from oracle import oracle as O
+
+    for st, g, hp in zip(states, grads, hps):
+        ost = O.OracleState(_np(st.weights.lp_values), _np(st.weights.corrections), _np(st.momentum.codes),
+                            _np(st.momentum.scales), None if st.variance is None else _np(st.variance.codes),
+                            None if st.variance is None else _np(st.variance.scales), st.t)
+        gf = g.float().numpy()
+        err = O.step_inplace(opt, ost, gf, **hp.__dict__)
+        assert err == 0
+        st.t += 1
+
+
+def _init_params(seed=0):
+    g = torch.Generator().manual_seed(seed)
+    return [(torch.randn(n, generator=g) * 0.02).to(torch.bfloat16) for n in SIZES]
+
+
+def _grads(step, seed=100):
+    g = torch.Generator().manual_seed(seed + step)
+    return [(torch.randn(n, generator=g) * 1e-3).to(torch.bfloat16) for n in SIZES]
+
+
+def _worker(rank, world, port, opt, q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2602_23349_b200 import optim as FO
+    from paper_2602_23349_b200.zero import ZeroFlashOptimizer
+
+    params = _init_params()
+    hp = {"adamw": [FO.AdamHyperParams(lr=1e-3, beta2=0.95, weight_decay=0.1), FO.AdamHyperParams(lr=1e-3)],
+          "sgd": [FO.SgdHyperParams(lr=0.1, weight_decay=1e-4), FO.SgdHyperParams(lr=0.1)],
+          "lion": [FO.LionHyperParams(lr=1e-4, weight_decay=0.1), FO.LionHyperParams(lr=1e-4)]}[opt]
+    zo = ZeroFlashOptimizer(params, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum")
+    for s in range(STEPS):
+        zo.zero_grad()
+        if rank == 0:
+            for p, g in zip(params, _grads(s)):
+                p.grad.copy_(g)
+        zo.step()
+    full = [p.detach().clone() for p in params]
+    shard_state = [(seg.param_index, seg.tensor_off, seg.length,
+                    {"rho": st.weights.corrections.numpy().copy(), "m": st.momentum.codes.numpy().copy(),
+                     "ms": st.momentum.scales.numpy().copy()}) for seg, st in zip(zo.segments, zo.states)]
+    q.put((rank, [_np(f).copy() for f in full], shard_state))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("opt", ["adamw", "sgd", "lion"])
+def test_zero1_matches_unsharded_oracle(opt, oracle_mod):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, opt, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict((r, (f, s)) for r, f, s in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # unsharded reference run
+    from paper_2602_23349_b200 import optim as FO
+
+    hp = {"adamw": [dict(lr=1e-3, beta2=0.95, weight_decay=0.1), dict(lr=1e-3)],
+          "sgd": [dict(lr=0.1, weight_decay=1e-4), dict(lr=0.1)],
+          "lion": [dict(lr=1e-4, weight_decay=0.1), dict(lr=1e-4)]}[opt]
+    hp = [{k: v for k, v in FO.HP_TYPES[opt](**h).__dict__.items()} for h in hp]
+    group_of = [0, 1, 0, 1, 1]
+    states = []
+    for p in _init_params():
+        lp = _np(p).copy()
+        n = lp.size
+        ng = -(-n // 32)
+        v = (np.zeros(n, np.uint8), np.zeros(ng, np.float16)) if opt == "adamw" else (None, None)
+        states.append(oracle_mod.OracleState(lp, np.zeros(n, np.int8), np.zeros(n, np.int8),
+                                             np.zeros(ng, np.float16), v[0], v[1], 0))
+    for s in range(STEPS):
+        for i, (st, g) in enumerate(zip(states, _grads(s))):
+            assert oracle_mod.step_inplace(opt, st, g.float().numpy(), **hp[group_of[i]]) == 0
+    for r in (0, 1):
+        full, shard_state = results[r]
+        for i, st in enumerate(states):
+            assert np.array_equal(full[i], st.lp), (r, i)
+        for pi, off, length, d in shard_state:
+            st = states[pi]
+            assert np.array_equal(d["rho"], st.rho[off:off + length])
+            assert np.array_equal(d["m"], st.m_codes[off:off + length])
+            g0 = off // 32
+            assert np.array_equal(d["ms"].view(np.uint16), st.m_scales[g0:g0 + d["ms"].size].view(np.uint16))
+    # the two shards together cover every element exactly once
+    cover = {}
+    for r in (0, 1):
+        for pi, off, length, _ in results[r][1]:
+            cover.setdefault(pi, []).append((off, length))
+    for pi, runs in cover.items():
+        runs.sort()
+        assert sum(ln for _, ln in runs) == SIZES[pi]
+        assert runs[0][0] == 0 and all(a + b == c for (a, b), (c, _) in zip(runs, runs[1:]))
