@@ -189,18 +189,30 @@ class FlashOptimizer(torch.optim.Optimizer):
         return sd
 
     def load_state_dict(self, state_dict: dict) -> None:
-        super().load_state_dict(state_dict)
-        for group in self.param_groups:
-            for p in group["params"]:
-                st = self.state[p]
-                for k in self._SCALES:
-                    if k in st:
-                        v = st[k]
-                        st[k] = v.view(torch.float16) if v.dtype == torch.int16 else v.to(torch.float16)
-                if "step" in st:
-                    st["step"] = int(st["step"])
-                if p.dtype == torch.float32:  # a fresh model: the checkpoint holds bf16 weights.lp
-                    p.data = p.data.to(torch.bfloat16)
+        # torch.optim casts every state tensor of a floating-point parameter to
+        # the parameter dtype; load the groups through torch and the state
+        # tensors directly, in their own dtypes.
+        saved = state_dict["state"]
+        super().load_state_dict({**state_dict, "state": {}})
+        id_map = {}
+        for g_saved, g in zip(state_dict["param_groups"], self.param_groups):
+            for pid, p in zip(g_saved["params"], g["params"]):
+                id_map[pid] = p
+        for pid, st in saved.items():
+            p = id_map[pid]
+            if p.dtype == torch.float32:  # a fresh model: the checkpoint holds bf16 weights.lp
+                p.data = p.data.to(torch.bfloat16)
+            new = {}
+            for k, v in st.items():
+                if isinstance(v, torch.Tensor):
+                    v = v.to(p.device, copy=True)  # deep copy, like torch.optim
+                    if k in self._SCALES and v.dtype == torch.int16:
+                        v = v.view(torch.float16)
+                new[k] = int(v) if k == "step" else v
+            self.state[p] = new
+        for g in self.param_groups:
+            for p in g["params"]:
+                self._init_state(p)
 
 
 class FlashAdamW(FlashOptimizer):
