@@ -330,7 +330,14 @@ def run_ours(args) -> None:
     peak, peak_kind = peaks()
     bpp = BYTES_PER_PARAM[opt]
     achieved = n_local * bpp / (avg_kern_ms * 1e-3) / 1e9
-    launches_per_step = len(plan.launch_groups()) if hasattr(plan, "launch_groups") else (len(sizes) + 383) // 384
+    launches_per_step = (len(sizes) + 383) // 384  # one hyper-parameter set, <= 384 tensors per launch
+    traffic = args.traffic
+    if traffic is None:
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f)["bytes_per_param"] * n_local / 1e9  # GB per launch
+        except Exception:
+            traffic = None
 
     e2e = None
     cpu = None
@@ -352,7 +359,8 @@ def run_ours(args) -> None:
                        else "L2-resident working set",
                        "parallelism": f"zero1-shard{world}" if world > 1 else "single-gpu"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": args.traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "GB per launch",
+                         "traffic_source": "profiles/ncu_traffic.json (ncu dram bytes per param x params)",
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "bytes_per_param": bpp, "kernel_ms": avg_kern_ms,
                          "kernel": "fo::step_tma_kernel (cuda events on the launch stream)"},
