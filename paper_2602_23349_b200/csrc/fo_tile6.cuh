@@ -1,0 +1,341 @@
+// fo_tile6.cuh -- the fused step's per-tile arithmetic (warp-specialised
+// kernel), included by fo_step_impl.cuh.
+//
+// Bit-identical to process_tile_exact (and therefore to the reference,
+// optim.py:385-459) whenever no guard trips; a tripped guard anywhere in the
+// warp sends the whole tile to process_tile_exact before anything is
+// stored.  Differences from compute_tile (the older kernels' tile):
+//
+//  * integer reconstruct (formats.py:248-276).  theta = RN(lp + RN(rho/127)
+//    * 2^ell) is lp's f32 bit pattern plus R(rho) = rint_even(RN(|rho|/127)
+//    * 2^15) ulps, moving away from zero when rho has lp's sign and toward
+//    zero otherwise.  lp has 16 zero low mantissa bits, so the tie parity
+//    is R's; 2^ell is exactly 2^15 f32 ulps of lp's binade, and at a binade
+//    bottom with rho pointing toward zero (the formats.py:147-154
+//    refinement) 2^(ell-1) is 2^15 ulps of the binade below, which integer
+//    subtraction on the bit pattern steps into.  Checked for every finite
+//    bf16 code x every rho (tests/test_gpu_primitives.py, test_tile6_
+//    reconstruct): the only mismatches are lp = +-0 with rho of the other
+//    sign (theta comes out NaN -> guard) and (-0, rho = 0) (theta comes out
+//    -0 where the reference has +0 -> guard on a -0 / zero update).
+//  * guards on the packed inputs with 16x2 SIMD min/max, and on the
+//    updated weights with float min/max of |theta_new|;
+//  * gradients stay packed bf16 words until the update.
+#pragma once
+// (textually included inside namespace fo)
+
+struct Luts6 {
+  int r[256];    // R(rho) by byte, signed; 0 for the invalid code -128 (caught by the rho guard)
+  float m[256];  // quantize.py:129-130, z/(2-|z|) for every int8 code (by byte)
+  float v[256];  // quantize.py:156, c/255
+};
+
+__device__ __forceinline__ void init_luts6(Luts6& L) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const int rho = (int)(int8_t)i;
+    L.r[i] = rho == -128 ? 0 : __float2int_rn(__fmul_rn(__fdiv_rn((float)rho, 127.0f), 32768.0f));
+    L.m[i] = momentum_unit(rho);
+    L.v[i] = variance_unit(i);
+  }
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// The exact recompute is rare (guards only trip on magnitudes training does
+// not produce); keeping it out of line keeps its register demand out of the
+// fast path's allocation.
+template <int OPT, typename GradT>
+__device__ __noinline__ void exact_tile_call(const TArg T, const fo_hparams h, int64_t base, int lane,
+                                             uint32_t* err_out) {
+  process_tile_exact<OPT, GradT, FEPL>(T, h, base, lane, err_out);
+}
+
+template <typename GradT>
+struct TileIn6 {
+  static constexpr int E = FEPL, NW = FEPL / 2, NB = FEPL / 4;
+  static constexpr int NG = sizeof(GradT) == 2 ? NW : E;  // grad words
+  uint32_t lw[NW], rw[NB], mw[NB], vw[NB], gw[NG];
+  uint32_t msb, vsb;
+};
+
+template <int OPT, typename GradT>
+__device__ __forceinline__ void load6_smem(const uint8_t* lp, const uint8_t* g, const uint8_t* rho, const uint8_t* mq,
+                                           const uint8_t* vq, const uint16_t* ms, const uint16_t* vs, int lane,
+                                           TileIn6<GradT>& in) {
+  constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
+  constexpr int E = FEPL, NW = E / 2, NB = E / 4, NG = TileIn6<GradT>::NG;
+  const int e = lane * E;
+#pragma unroll
+  for (int c = 0; c < NW / 4; ++c) {
+    const uint4 a = *reinterpret_cast<const uint4*>(lp + 2 * e + 16 * c);
+    in.lw[4 * c] = a.x; in.lw[4 * c + 1] = a.y; in.lw[4 * c + 2] = a.z; in.lw[4 * c + 3] = a.w;
+  }
+#pragma unroll
+  for (int c = 0; c < NG / 4; ++c) {
+    const uint4 a = *reinterpret_cast<const uint4*>(g + sizeof(GradT) * e + 16 * c);
+    in.gw[4 * c] = a.x; in.gw[4 * c + 1] = a.y; in.gw[4 * c + 2] = a.z; in.gw[4 * c + 3] = a.w;
+  }
+  auto bytes = [&](const uint8_t* src, uint32_t* wd) {
+    if (NB == 4) {
+      const uint4 a = *reinterpret_cast<const uint4*>(src + e);
+      wd[0] = a.x; wd[1] = a.y; wd[2] = a.z; wd[3] = a.w;
+    } else {
+      const uint2 a = *reinterpret_cast<const uint2*>(src + e);
+      wd[0] = a.x; wd[1] = a.y;
+    }
+  };
+  bytes(rho, in.rw);
+  bytes(mq, in.mw);
+  if (ADAM) bytes(vq, in.vw);
+  in.msb = ms[e / GROUP];
+  in.vsb = ADAM ? vs[e / GROUP] : 0u;
+}
+
+// Partial (or unaligned) tile straight from global memory; elements past n
+// read as zero state with zero gradient.
+template <int OPT, typename GradT>
+__device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int lane, TileIn6<GradT>& in) {
+  constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
+  constexpr int E = FEPL, NW = E / 2, NB = E / 4, NG = TileIn6<GradT>::NG;
+  const int64_t n = T.n;
+  const int64_t e0 = base + (int64_t)lane * E;
+#pragma unroll
+  for (int q = 0; q < NW; ++q) in.lw[q] = 0;
+#pragma unroll
+  for (int q = 0; q < NG; ++q) in.gw[q] = 0;
+#pragma unroll
+  for (int q = 0; q < NB; ++q) in.rw[q] = in.mw[q] = in.vw[q] = 0;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int64_t i = e0 + j;
+    if (i < n) {
+      in.lw[j >> 1] |= (uint32_t)T.lp[i] << (16 * (j & 1));
+      in.rw[j >> 2] |= (uint32_t)(uint8_t)T.rho[i] << (8 * (j & 3));
+      in.mw[j >> 2] |= (uint32_t)(uint8_t)T.mq[i] << (8 * (j & 3));
+      if (ADAM) in.vw[j >> 2] |= (uint32_t)T.vq[i] << (8 * (j & 3));
+      if (sizeof(GradT) == 2)
+        in.gw[j >> 1] |= (uint32_t)reinterpret_cast<const uint16_t*>(T.g)[i] << (16 * (j & 1));
+      else
+        in.gw[j] = reinterpret_cast<const uint32_t*>(T.g)[i];
+    }
+  }
+  in.msb = e0 < n ? (uint32_t)T.ms[e0 >> 5] : 0u;
+  in.vsb = (ADAM && e0 < n) ? (uint32_t)T.vs[e0 >> 5] : 0u;
+}
+
+template <int OPT, typename GradT, int BC>
+__device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h, int64_t base, int lane,
+                                              uint32_t& err, const Luts6& L, float negzero, uint32_t* err_out,
+                                              bool full, const TileIn6<GradT>& in) {
+  using namespace fast;
+  constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
+  constexpr int E = FEPL, NW = E / 2, NB = E / 4, LPG = GROUP / E;
+  // Every product that feeds an addition is an FFMA2 with this run-time -0:
+  // RN(a*b + -0) == RN(a*b) bit for bit, and ptxas cannot contract it into
+  // the following add (it does contract plain f32x2 mul+add, .rn or not).
+  const float2 Z = dup(negzero);
+  const int64_t n = T.n;
+  const int64_t e0 = base + (int64_t)lane * E;
+
+  // ---- input guards (packed) ----
+  // gradients: 0 < |g| < 2^-35 (the fast divisions / square roots rely on
+  // every nonzero m, v being far from the underflow range)
+  bool bad = false;
+  if (sizeof(GradT) == 2) {
+    uint32_t gmin = 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) gmin = __vminu2(gmin, __vsub2(in.gw[k] & 0x7FFF7FFFu, 0x00010001u));
+    bad |= __vcmpltu2(gmin, 0x2DFF2DFFu) != 0;
+  } else {
+    uint32_t gmin = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < E; ++j) gmin = min(gmin, in.gw[j] * 2u - 1u);
+    bad |= gmin < (0x2E000000u * 2u - 1u);
+  }
+  // rho == -128 (formats.py:270-271): as signed 16-bit lanes, a word whose
+  // high byte is 0x80 is below -32512; the shifted copy covers the low bytes.
+  {
+    uint32_t rmin = 0x7FFF7FFFu;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) rmin = __vmins2(rmin, __vmins2(in.rw[c], in.rw[c] << 8));
+    bad |= __vcmplts2(rmin, 0x81008100u) != 0;
+  }
+  // A non-finite input scale makes every dequantised value of its group
+  // non-finite (quantize.py:131,157): exact path.
+  bad |= (in.msb & 0x7C00u) == 0x7C00u;
+  if (ADAM) bad |= (in.vsb & 0x7C00u) == 0x7C00u;
+
+  // ---- per pair: reconstruct, dequantise, update, split ----
+  // One pass per pair keeps only m, the variance root and the packed
+  // outputs live across the tile (the group maxima need all 16 elements).
+  const float msf = half_bits_to_float(in.msb);
+  const float vsf = half_bits_to_float(in.vsb);
+  float m[E], root[E];
+  uint32_t cw[NW], ro[NB];
+  float tmin = 3.0e38f, tmax = 0.0f;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    const int j = 2 * k;
+    const uint32_t w = in.lw[k];
+    // reconstruct (formats.py:248-276), see the header comment
+    const uint32_t lpl = w << 16, lph = w & 0xFFFF0000u;
+    const int sl = (int)lpl >> 31, sh = (int)w >> 31;
+    const int rl = L.r[prmt(in.rw[j >> 2], 0, 0x4440u + (j & 3))];
+    const int rh = L.r[prmt(in.rw[j >> 2], 0, 0x4440u + (j & 3) + 1)];
+    const float2 th2 = make_float2(__uint_as_float(lpl + (uint32_t)((rl ^ sl) - sl)),
+                                   __uint_as_float(lph + (uint32_t)((rh ^ sh) - sh)));
+    // dequantise (quantize.py:125-131, :152-158)
+    const float2 u2 = make_float2(L.m[prmt(in.mw[j >> 2], 0, 0x4440u + (j & 3))],
+                                  L.m[prmt(in.mw[j >> 2], 0, 0x4440u + (j & 3) + 1)]);
+    const float2 mp2 = fma2(u2, dup(msf), Z);
+    float2 g2;
+    if (sizeof(GradT) == 2) g2 = make_float2(__uint_as_float(in.gw[k] << 16), __uint_as_float(in.gw[k] & 0xFFFF0000u));
+    else g2 = make_float2(__uint_as_float(in.gw[j]), __uint_as_float(in.gw[j + 1]));
+    // update (optim.py:393-396, :418-424, :445-447)
+    float2 m2, tn2;
+    if (OPT == FO_OPT_ADAMW) {
+      const float2 z2 = make_float2(L.v[prmt(in.vw[j >> 2], 0, 0x4440u + (j & 3))],
+                                    L.v[prmt(in.vw[j >> 2], 0, 0x4440u + (j & 3) + 1)]);
+      const float2 r2 = fma2(z2, dup(vsf), Z);
+      const float2 vp2 = fma2(r2, r2, Z);
+      m2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
+      const float2 v2 = add2(fma2(dup(h.b2), vp2, Z), fma2(dup(h.omb2), fma2(g2, g2, Z), Z));
+      const float2 mh = (BC & 1) ? m2 : div_y(m2, dup(h.bc1), dup(h.rbc1));
+      float2 rt2;  // RN(sqrt(v)), also quantize.py:145
+      float2 den;
+      if (BC & 2) {
+        rt2 = sqrt_rn2(v2);
+        den = add2(rt2, dup(h.eps));
+      } else {
+        rt2 = sqrt_rn2(v2);
+        den = add2(sqrt_rn2(div_y(v2, dup(h.bc2), dup(h.rbc2))), dup(h.eps));
+      }
+      root[j] = rt2.x;
+      root[j + 1] = rt2.y;
+      const float2 u = add2(div_rn2(mh, den), fma2(dup(h.wd), th2, Z));
+      tn2 = add2(th2, neg2(fma2(dup(h.lr), u, Z)));
+    } else if (OPT == FO_OPT_SGD) {
+      m2 = add2(fma2(dup(h.mu), mp2, Z), g2);
+      const float2 u = add2(m2, fma2(dup(h.wd), th2, Z));
+      tn2 = add2(th2, neg2(fma2(dup(h.lr), u, Z)));
+    } else {
+      const float2 c2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
+      float2 s2;  // np.sign with sign(+-0) = +0 (c is never -0 here)
+      s2.x = c2.x > 0.0f ? 1.0f : (c2.x < 0.0f ? -1.0f : (c2.x != c2.x ? c2.x : 0.0f));
+      s2.y = c2.y > 0.0f ? 1.0f : (c2.y < 0.0f ? -1.0f : (c2.y != c2.y ? c2.y : 0.0f));
+      m2 = add2(fma2(dup(h.b2), mp2, Z), fma2(dup(h.omb2), g2, Z));
+      const float2 u = add2(s2, fma2(dup(h.wd), th2, Z));
+      tn2 = add2(th2, neg2(fma2(dup(h.lr), u, Z)));
+    }
+    m[j] = m2.x;
+    m[j + 1] = m2.y;
+    // split (formats.py:232-245)
+    __nv_bfloat162 c2 = __floats2bfloat162_rn(tn2.x, tn2.y);  // RNE, overflow -> inf
+    cw[k] = *reinterpret_cast<uint32_t*>(&c2);
+    const float2 lp2 = make_float2(__uint_as_float(cw[k] << 16), __uint_as_float(cw[k] & 0xFFFF0000u));
+    const float2 e2 = add2(tn2, neg2(lp2));  // exact residual
+    // K = 127 * 2^-ell with ell = expf(theta) - 135: the binade-bottom rule is
+    // implied by theta's own exponent; valid for expf(theta) in [14, 254].
+    const float2 k2 = make_float2(__uint_as_float(0x867E0000u - (__float_as_uint(tn2.x) & 0x7F800000u)),
+                                  __uint_as_float(0x867E0000u - (__float_as_uint(tn2.y) & 0x7F800000u)));
+    // e*K is exact (<= 24 significant bits), so adding 1.5*2^23 in the same
+    // FFMA2 leaves rint(e*K) (ties-to-even) in the low mantissa bits.
+    const float2 q2 = fma2(e2, k2, dup(12582912.0f));
+    const uint32_t pr = prmt(__float_as_uint(q2.x), __float_as_uint(q2.y), 0x0040u);  // two codes -> bytes 0, 1
+    if (k & 1) ro[k >> 1] = prmt(ro[k >> 1], pr, 0x5410u);
+    else ro[k >> 1] = pr;
+    tmin = fminf(tmin, fminf(fabsf(tn2.x), fabsf(tn2.y)));
+    tmax = maxnan3(tmax, fabsf(tn2.x), fabsf(tn2.y));
+  }
+  // |theta_new| in [2^-113, bf16 max): the split's exponent rule holds, and
+  // the reconstruct's zero cases (NaN, or a zero whose sign may differ from
+  // the reference's) are excluded.  NaN fails both comparisons.
+  bad |= !(tmin >= 0x1p-113f) || !(tmax < 0x1.FFp127f);
+
+  // ---- epilogue: momentum (quantize.py:109-122), exact ----
+  float amax = 0.0f;
+#pragma unroll
+  for (int j = 0; j < E; j += 2) amax = maxnan3(amax, fabsf(m[j]), fabsf(m[j + 1]));
+#pragma unroll
+  for (int o = 1; o < LPG; o <<= 1) amax = maxnan(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  bad |= !(amax <= 65504.0f);  // non-finite m or scale overflow: exact path reports it
+  const uint32_t new_msb = (uint32_t)__half_as_ushort(__float2half_ru(amax));
+  uint32_t mo[NB];
+  {
+    const float s = half_bits_to_float(new_msb);
+    const float den = (s == 0.0f) ? 1.0f : s;
+    const float y = rcp_rn_normal(den);
+#pragma unroll
+    for (int j = 0; j < E; j += 2) {
+      const float2 mn = div_y(make_float2(m[j], m[j + 1]), dup(den), dup(y));  // RN(m/s)
+      const float2 d = make_float2(__fadd_rn(1.0f, fabsf(mn.x)), __fadd_rn(1.0f, fabsf(mn.y)));
+      // RN(2m'/(1+|m'|)) = 2*RN(m'/(1+|m'|)) (power-of-two scaling), so
+      // RN(z*127) = RN(RN(m'/d)*254)
+      const float2 zh = div_rn2(mn, d);
+      const float2 t = add2(fma2(zh, dup(254.0f), Z), dup(12582912.0f));  // rint(RN(z*127))
+      const uint32_t pr = prmt(__float_as_uint(t.x), __float_as_uint(t.y), 0x0040u);
+      if (j & 2) mo[j >> 2] = prmt(mo[j >> 2], pr, 0x5410u);
+      else mo[j >> 2] = pr;
+    }
+  }
+
+  // ---- epilogue: variance (quantize.py:134-149), exact ----
+  uint32_t new_vsb = 0, vo[NB];
+  if (ADAM) {
+    float rmax = 0.0f;
+#pragma unroll
+    for (int j = 0; j < E; j += 2) rmax = maxnan3(rmax, root[j], root[j + 1]);
+#pragma unroll
+    for (int o = 1; o < LPG; o <<= 1) rmax = maxnan(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    bad |= !(rmax <= 65504.0f);
+    new_vsb = (uint32_t)__half_as_ushort(__float2half_ru(rmax));
+    const float s = half_bits_to_float(new_vsb);
+    const float den = (s == 0.0f) ? 1.0f : s;
+    const float y = rcp_rn_normal(den);
+#pragma unroll
+    for (int j = 0; j < E; j += 2) {
+      const float2 vn = div_y(make_float2(root[j], root[j + 1]), dup(den), dup(y));  // RN(r/s)
+      const float2 t = add2(fma2(vn, dup(255.0f), Z), dup(12582912.0f));           // rint(RN(vn*255))
+      const uint32_t pr = prmt(__float_as_uint(t.x), __float_as_uint(t.y), 0x0040u);
+      if (j & 2) vo[j >> 2] = prmt(vo[j >> 2], pr, 0x5410u);
+      else vo[j >> 2] = pr;
+    }
+  }
+
+  // ---- any guard tripped anywhere in the warp: recompute the tile exactly ----
+  if (__any_sync(0xffffffffu, bad)) {
+    exact_tile_call<OPT, GradT>(T, h, base, lane, err_out);
+    return;
+  }
+
+  // ---- stores ----
+  if (full) {
+#pragma unroll
+    for (int c = 0; c < NW / 4; ++c)
+      stcs4(T.lp + e0 + 8 * c, make_uint4(cw[4 * c], cw[4 * c + 1], cw[4 * c + 2], cw[4 * c + 3]));
+    store_bytes<NB>(T.rho + e0, ro);
+    store_bytes<NB>(T.mq + e0, mo);
+    if (ADAM) store_bytes<NB>(T.vq + e0, vo);
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int64_t i = e0 + j;
+      if (i < n) {
+        T.lp[i] = (uint16_t)(cw[j >> 1] >> (16 * (j & 1)));
+        T.rho[i] = (int8_t)(ro[j >> 2] >> (8 * (j & 3)));
+        T.mq[i] = (int8_t)(mo[j >> 2] >> (8 * (j & 3)));
+        if (ADAM) T.vq[i] = (uint8_t)(vo[j >> 2] >> (8 * (j & 3)));
+      }
+    }
+  }
+  if ((lane & (LPG - 1)) == 0 && e0 < n) {
+    T.ms[e0 >> 5] = (uint16_t)new_msb;
+    if (ADAM) T.vs[e0 >> 5] = (uint16_t)new_vsb;
+  }
+  (void)err;
+}
+
