@@ -58,7 +58,9 @@ def dist_env() -> tuple[int, int, int]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / power / throttle reasons sampled every 50 ms during
+    the timed region.  start() returns once the first sample has arrived, so
+    the samples cover the timed steps rather than nvidia-smi's start-up."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -67,37 +69,62 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.lines: list[str] = []
+        self.mark = 0
 
     def start(self):
+        import threading
+
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
+
+        def pump():
+            for line in self.proc.stdout:
+                self.lines.append(line)
+
+        threading.Thread(target=pump, daemon=True).start()
+        t = time.time()
+        while not self.lines and time.time() - t < 10:
+            time.sleep(0.02)
+
+    def begin(self):
+        """Mark the start of the timed region (samples before it are dropped)."""
+        self.mark = len(self.lines)
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        sms, maxs, reasons = [], [], set()
+        try:
+            self.proc.wait(timeout=10)
+        except Exception:
+            pass
+        lines = self.lines[self.mark:] or self.lines[-1:]
+        sms, maxs, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
             try:
                 sms.append(float(f[1]))
                 maxs.append(float(f[2]))
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for nm, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         sms.sort()
+        pw.sort()
         return {"sm_mhz": sms[len(sms) // 2] if sms else None, "sm_max_mhz": max(maxs) if maxs else None,
-                "reasons": sorted(reasons), "samples": len(sms)}
+                "power_w": pw[len(pw) // 2] if pw else None, "reasons": sorted(reasons), "samples": len(sms)}
 
 
 def cpu_sample_run(opt: str, config: str, target_s: float, nthreads: int) -> dict:
@@ -289,19 +316,20 @@ def run_ours(args) -> None:
         t = fl.states[0].t + 1
         plan.launch([hp.scalars(t)], err.data_ptr(), sh)
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    clocks.begin()
     t0.record(stream)
     for i in range(args.steps):
         ev[i][0].record(stream)
@@ -363,7 +391,7 @@ def run_ours(args) -> None:
                          "traffic_source": "profiles/ncu_traffic.json (ncu dram bytes per param x params)",
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "bytes_per_param": bpp, "kernel_ms": avg_kern_ms,
-                         "kernel": "fo::step_tma_kernel (cuda events on the launch stream)"},
+                         "kernel": "fo::step_ws_kernel (cuda events on the launch stream)"},
             "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clk, "gpu_launches": args.steps * launches_per_step,
             "device_errors": emask,

@@ -127,10 +127,57 @@ __device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int la
   in.vsb = (ADAM && e0 < n) ? (uint32_t)T.vs[e0 >> 5] : 0u;
 }
 
-template <int OPT, typename GradT, int BC>
+// Sources of one lane's 16 elements, read half (8 elements) at a time so
+// only half of the packed inputs is live at once.
+template <int OPT, typename GradT>
+struct SmemSrc {  // a full tile in the stage ring (read in place)
+  static constexpr int NGH = TileIn6<GradT>::NG / 2;
+  const uint8_t *lp, *g, *rho, *mq, *vq;
+  uint32_t msb, vsb;
+  __device__ __forceinline__ void half(int h, uint32_t* lw, uint32_t* gw, uint32_t* rw, uint32_t* mw,
+                                       uint32_t* vw) const {
+    const uint4 a = *reinterpret_cast<const uint4*>(lp + 16 * h);
+    lw[0] = a.x; lw[1] = a.y; lw[2] = a.z; lw[3] = a.w;
+#pragma unroll
+    for (int c = 0; c < NGH / 4; ++c) {
+      const uint4 b = *reinterpret_cast<const uint4*>(g + 4 * NGH * h + 16 * c);
+      gw[4 * c] = b.x; gw[4 * c + 1] = b.y; gw[4 * c + 2] = b.z; gw[4 * c + 3] = b.w;
+    }
+    const uint2 r = *reinterpret_cast<const uint2*>(rho + 8 * h);
+    rw[0] = r.x; rw[1] = r.y;
+    const uint2 m = *reinterpret_cast<const uint2*>(mq + 8 * h);
+    mw[0] = m.x; mw[1] = m.y;
+    if (OPT == FO_OPT_ADAMW) {
+      const uint2 v = *reinterpret_cast<const uint2*>(vq + 8 * h);
+      vw[0] = v.x; vw[1] = v.y;
+    }
+  }
+};
+
+template <typename GradT>
+struct RegSrc {  // a partial tile already gathered into registers
+  static constexpr int NGH = TileIn6<GradT>::NG / 2;
+  const TileIn6<GradT>& in;
+  uint32_t msb, vsb;
+  __device__ __forceinline__ void half(int h, uint32_t* lw, uint32_t* gw, uint32_t* rw, uint32_t* mw,
+                                       uint32_t* vw) const {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) lw[q] = in.lw[4 * h + q];
+#pragma unroll
+    for (int q = 0; q < NGH; ++q) gw[q] = in.gw[NGH * h + q];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      rw[q] = in.rw[2 * h + q];
+      mw[q] = in.mw[2 * h + q];
+      vw[q] = in.vw[2 * h + q];
+    }
+  }
+};
+
+template <int OPT, typename GradT, int BC, class Src>
 __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h, int64_t base, int lane,
                                               uint32_t& err, const Luts6& L, float negzero, uint32_t* err_out,
-                                              bool full, const TileIn6<GradT>& in) {
+                                              bool full, const Src& in) {
   using namespace fast;
   constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
   constexpr int E = FEPL, NW = E / 2, NB = E / 4, LPG = GROUP / E;
@@ -141,29 +188,13 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   const int64_t n = T.n;
   const int64_t e0 = base + (int64_t)lane * E;
 
-  // ---- input guards (packed) ----
+  // ---- input guards (accumulated over the packed inputs in the loop) ----
   // gradients: 0 < |g| < 2^-35 (the fast divisions / square roots rely on
-  // every nonzero m, v being far from the underflow range)
+  // every nonzero m, v being far from the underflow range); rho == -128
+  // (formats.py:270-271): as signed 16-bit lanes, a word whose high byte is
+  // 0x80 is below -32512, and the shifted copy covers the low bytes.
   bool bad = false;
-  if (sizeof(GradT) == 2) {
-    uint32_t gmin = 0xFFFFFFFFu;
-#pragma unroll
-    for (int k = 0; k < NW; ++k) gmin = __vminu2(gmin, __vsub2(in.gw[k] & 0x7FFF7FFFu, 0x00010001u));
-    bad |= __vcmpltu2(gmin, 0x2DFF2DFFu) != 0;
-  } else {
-    uint32_t gmin = 0xFFFFFFFFu;
-#pragma unroll
-    for (int j = 0; j < E; ++j) gmin = min(gmin, in.gw[j] * 2u - 1u);
-    bad |= gmin < (0x2E000000u * 2u - 1u);
-  }
-  // rho == -128 (formats.py:270-271): as signed 16-bit lanes, a word whose
-  // high byte is 0x80 is below -32512; the shifted copy covers the low bytes.
-  {
-    uint32_t rmin = 0x7FFF7FFFu;
-#pragma unroll
-    for (int c = 0; c < NB; ++c) rmin = __vmins2(rmin, __vmins2(in.rw[c], in.rw[c] << 8));
-    bad |= __vcmplts2(rmin, 0x81008100u) != 0;
-  }
+  uint32_t gmin = 0xFFFFFFFFu, rmin = 0x7FFF7FFFu;
   // A non-finite input scale makes every dequantised value of its group
   // non-finite (quantize.py:131,157): exact path.
   bad |= (in.msb & 0x7C00u) == 0x7C00u;
@@ -177,29 +208,46 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   float m[E], root[E];
   uint32_t cw[NW], ro[NB];
   float tmin = 3.0e38f, tmax = 0.0f;
+  constexpr int NGH = TileIn6<GradT>::NG / 2;
+  uint32_t hl[4], hg[NGH], hr[2], hm[2], hv[2];
 #pragma unroll
   for (int k = 0; k < NW; ++k) {
     const int j = 2 * k;
-    const uint32_t w = in.lw[k];
+    if ((k & 3) == 0) {
+      in.half(k >> 2, hl, hg, hr, hm, hv);
+      if (sizeof(GradT) == 2) {
+#pragma unroll
+        for (int q = 0; q < NGH; ++q) gmin = __vminu2(gmin, __vsub2(hg[q] & 0x7FFF7FFFu, 0x00010001u));
+      } else {
+#pragma unroll
+        for (int q = 0; q < NGH; ++q) gmin = min(gmin, hg[q] * 2u - 1u);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) rmin = __vmins2(rmin, __vmins2(hr[q], hr[q] << 8));
+    }
+    const uint32_t w = hl[k & 3];
+    const uint32_t rwd = hr[(j >> 2) & 1], mwd = hm[(j >> 2) & 1], vwd = hv[(j >> 2) & 1];
     // reconstruct (formats.py:248-276), see the header comment
     const uint32_t lpl = w << 16, lph = w & 0xFFFF0000u;
     const int sl = (int)lpl >> 31, sh = (int)w >> 31;
-    const int rl = L.r[prmt(in.rw[j >> 2], 0, 0x4440u + (j & 3))];
-    const int rh = L.r[prmt(in.rw[j >> 2], 0, 0x4440u + (j & 3) + 1)];
+    const int rl = L.r[prmt(rwd, 0, 0x4440u + (j & 3))];
+    const int rh = L.r[prmt(rwd, 0, 0x4440u + (j & 3) + 1)];
     const float2 th2 = make_float2(__uint_as_float(lpl + (uint32_t)((rl ^ sl) - sl)),
                                    __uint_as_float(lph + (uint32_t)((rh ^ sh) - sh)));
     // dequantise (quantize.py:125-131, :152-158)
-    const float2 u2 = make_float2(L.m[prmt(in.mw[j >> 2], 0, 0x4440u + (j & 3))],
-                                  L.m[prmt(in.mw[j >> 2], 0, 0x4440u + (j & 3) + 1)]);
+    const float2 u2 = make_float2(L.m[prmt(mwd, 0, 0x4440u + (j & 3))], L.m[prmt(mwd, 0, 0x4440u + (j & 3) + 1)]);
     const float2 mp2 = fma2(u2, dup(msf), Z);
     float2 g2;
-    if (sizeof(GradT) == 2) g2 = make_float2(__uint_as_float(in.gw[k] << 16), __uint_as_float(in.gw[k] & 0xFFFF0000u));
-    else g2 = make_float2(__uint_as_float(in.gw[j]), __uint_as_float(in.gw[j + 1]));
+    if (sizeof(GradT) == 2) {
+      const uint32_t gwd = hg[k & 3];
+      g2 = make_float2(__uint_as_float(gwd << 16), __uint_as_float(gwd & 0xFFFF0000u));
+    } else {
+      g2 = make_float2(__uint_as_float(hg[j & 7]), __uint_as_float(hg[(j & 7) + 1]));
+    }
     // update (optim.py:393-396, :418-424, :445-447)
     float2 m2, tn2;
     if (OPT == FO_OPT_ADAMW) {
-      const float2 z2 = make_float2(L.v[prmt(in.vw[j >> 2], 0, 0x4440u + (j & 3))],
-                                    L.v[prmt(in.vw[j >> 2], 0, 0x4440u + (j & 3) + 1)]);
+      const float2 z2 = make_float2(L.v[prmt(vwd, 0, 0x4440u + (j & 3))], L.v[prmt(vwd, 0, 0x4440u + (j & 3) + 1)]);
       const float2 r2 = fma2(z2, dup(vsf), Z);
       const float2 vp2 = fma2(r2, r2, Z);
       m2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
@@ -255,6 +303,9 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   // the reconstruct's zero cases (NaN, or a zero whose sign may differ from
   // the reference's) are excluded.  NaN fails both comparisons.
   bad |= !(tmin >= 0x1p-113f) || !(tmax < 0x1.FFp127f);
+  if (sizeof(GradT) == 2) bad |= __vcmpltu2(gmin, 0x2DFF2DFFu) != 0;
+  else bad |= gmin < (0x2E000000u * 2u - 1u);
+  bad |= __vcmplts2(rmin, 0x81008100u) != 0;
 
   // ---- epilogue: momentum (quantize.py:109-122), exact ----
   float amax = 0.0f;
