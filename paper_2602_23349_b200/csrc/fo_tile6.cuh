@@ -228,12 +228,13 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const uint32_t w = hl[k & 3];
     const uint32_t rwd = hr[(j >> 2) & 1], mwd = hm[(j >> 2) & 1], vwd = hv[(j >> 2) & 1];
     // reconstruct (formats.py:248-276), see the header comment
+    // lp +- R as one IMAD: the direction is +1 for lp >= 0 and -1 for
+    // lp < 0 ((bits >> 30) | 1 with an arithmetic shift)
     const uint32_t lpl = w << 16, lph = w & 0xFFFF0000u;
-    const int sl = (int)lpl >> 31, sh = (int)w >> 31;
+    const int sl = ((int)lpl >> 30) | 1, sh = ((int)w >> 30) | 1;
     const int rl = L.r[prmt(rwd, 0, 0x4440u + (j & 3))];
     const int rh = L.r[prmt(rwd, 0, 0x4440u + (j & 3) + 1)];
-    const float2 th2 = make_float2(__uint_as_float(lpl + (uint32_t)((rl ^ sl) - sl)),
-                                   __uint_as_float(lph + (uint32_t)((rh ^ sh) - sh)));
+    const float2 th2 = make_float2(__uint_as_float(lpl + (uint32_t)(rl * sl)), __uint_as_float(lph + (uint32_t)(rh * sh)));
     // dequantise (quantize.py:125-131, :152-158)
     const float2 u2 = make_float2(L.m[prmt(mwd, 0, 0x4440u + (j & 3))], L.m[prmt(mwd, 0, 0x4440u + (j & 3) + 1)]);
     const float2 mp2 = fma2(u2, dup(msf), Z);
