@@ -187,6 +187,29 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   const float2 Z = dup(negzero);
   const int64_t n = T.n;
   const int64_t e0 = base + (int64_t)lane * E;
+#ifdef FO_COPY_ONLY
+  // bandwidth/power experiment: same loads and stores, no arithmetic
+  if (full) {
+    uint32_t hl[4], hg[TileIn6<GradT>::NG / 2], hr[2], hm[2], hv[2], a[8], b[4], c[4], d[4];
+    for (int hh = 0; hh < 2; ++hh) {
+      in.half(hh, hl, hg, hr, hm, hv);
+      for (int q = 0; q < 4; ++q) a[4 * hh + q] = hl[q] ^ hg[q & (TileIn6<GradT>::NG / 2 - 1)];
+      b[2 * hh] = hr[0]; b[2 * hh + 1] = hr[1];
+      c[2 * hh] = hm[0]; c[2 * hh + 1] = hm[1];
+      d[2 * hh] = hv[0]; d[2 * hh + 1] = hv[1];
+    }
+    stcs4(T.lp + e0, make_uint4(a[0], a[1], a[2], a[3]));
+    stcs4(T.lp + e0 + 8, make_uint4(a[4], a[5], a[6], a[7]));
+    store_bytes<4>(T.rho + e0, b);
+    store_bytes<4>(T.mq + e0, c);
+    if (ADAM) store_bytes<4>(T.vq + e0, d);
+    if ((lane & 1) == 0) {
+      T.ms[e0 >> 5] = (uint16_t)in.msb;
+      if (ADAM) T.vs[e0 >> 5] = (uint16_t)in.vsb;
+    }
+    return;
+  }
+#endif
 
   // ---- input guards (accumulated over the packed inputs in the loop) ----
   // gradients: 0 < |g| < 2^-35 (the fast divisions / square roots rely on
