@@ -323,6 +323,8 @@ def load_optimizer(optimizer, directory) -> None:
     params = [p for g in optimizer.param_groups for p in g["params"]]
     if len(params) != len(manifest["params"]):
         raise CheckpointError("parameter count differs from the checkpoint")
+    if hasattr(optimizer, "_plans"):
+        optimizer._plans = {}  # cached launch tables point at the replaced state tensors
     with torch.no_grad():
         for p, ent in zip(params, manifest["params"]):
             if list(p.shape) != ent["shape"]:

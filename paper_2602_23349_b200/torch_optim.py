@@ -141,6 +141,47 @@ class FlashOptimizer(torch.optim.Optimizer):
         for p in params:
             self.state[p]["step"] = int(self.state[p]["step"]) + 1
 
+    def _launch_cached(self, gi: int, group: dict, ps: list) -> bool:
+        """Fast path for the common case (every parameter of the group has a
+        contiguous bf16 gradient and the same step counter): the fo_tensor
+        table is built once per group and only gradient pointers change per
+        step.  Returns False when the general path must run."""
+        t0 = int(self.state[ps[0]]["step"])
+        grads = []
+        for p in ps:
+            g = p.grad
+            if g.dtype != torch.bfloat16 or not g.is_contiguous() or int(self.state[p]["step"]) != t0:
+                return False
+            grads.append(g)
+        key = (tuple(id(p) for p in ps), tuple(p.data_ptr() for p in ps))
+        plan = self._plans.get(gi)
+        if plan is None or plan[0] != key:
+            adam = self.OPT == "adamw"
+            table = (_lib.fo_tensor * len(ps))()
+            for i, p in enumerate(ps):
+                st, e = self.state[p], table[i]
+                e.lp = p.data.data_ptr()
+                e.rho = st["weights.rho"].data_ptr()
+                e.m_codes = st["momentum.codes"].data_ptr()
+                e.m_scales = st["momentum.scales"].data_ptr()
+                e.v_codes = st["variance.codes"].data_ptr() if adam else None
+                e.v_scales = st["variance.scales"].data_ptr() if adam else None
+                e.n = p.numel()
+                e.hp_index = 0
+            plan = (key, table)
+            self._plans[gi] = plan
+        table = plan[1]
+        for i, g in enumerate(grads):
+            table[i].grad = g.data_ptr()
+        hp = (_lib.fo_hparams * 1)(self.hp(group).scalars(t0 + 1))
+        dev = ps[0].device
+        _lib.check(_lib.lib().fo_step_mt(
+            _lib.OPT_TAGS[self.OPT], table, len(ps), hp, 1, _lib.FO_GRAD_BF16, 8, self.spec.group_size,
+            _lib.FO_VAR_COMPANDED, self._errors.ptr, stream_handle(dev)), "fo_step_mt")
+        for p in ps:
+            self.state[p]["step"] = t0 + 1
+        return True
+
     @torch.no_grad()
     def step(self, closure=None):
         loss = None
@@ -148,14 +189,15 @@ class FlashOptimizer(torch.optim.Optimizer):
             with torch.enable_grad():
                 loss = closure()
         dev = None
-        for group in self.param_groups:
+        for gi, group in enumerate(self.param_groups):
             ps = [p for p in group["params"] if p.grad is not None]
             if not ps:
                 continue
             dev = ps[0].device
             if self._errors is None or self._errors.word.device != dev:
                 self._errors = DeviceErrors(dev)
-            self._launch(ps, [p.grad.reshape(-1) for p in ps], group)
+            if not self._launch_cached(gi, group, ps):
+                self._launch(ps, [p.grad.reshape(-1) for p in ps], group)
         if self.check_errors and dev is not None:
             self.raise_errors()
         return loss
@@ -193,6 +235,7 @@ class FlashOptimizer(torch.optim.Optimizer):
         # the parameter dtype; load the groups through torch and the state
         # tensors directly, in their own dtypes.
         saved = state_dict["state"]
+        self._plans = {}
         super().load_state_dict({**state_dict, "state": {}})
         id_map = {}
         for g_saved, g in zip(state_dict["param_groups"], self.param_groups):
