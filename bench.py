@@ -274,6 +274,50 @@ def host_e2e(fl, grads_flat, opt, hp, t0, steps, warmup):
             "host_setup_s": round(alloc_s, 1)}
 
 
+def zero1_exchange(n_total: int, world: int, dev, stream, step_ms: float, args) -> dict:
+    """The ZeRO-1 exchange around the sharded step (paper_2602_23349_b200/zero.py):
+    NCCL reduce-scatter of the flat bf16 gradients into this rank's shard and
+    all-gather of the updated bf16 shard into the flat parameters, timed with
+    CUDA events (max over ranks).  In training the reduce-scatter replaces
+    DDP's all-reduce, so it is reported beside the step, not inside `value`."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_23349_b200.zero import ALIGN
+
+    unit = ALIGN * world
+    total = -(-n_total // unit) * unit
+    shard = total // world
+    flat = torch.empty(total, dtype=torch.bfloat16, device=dev)
+    flat.normal_(0, 1e-3)
+    part = torch.empty(shard, dtype=torch.bfloat16, device=dev)
+    iters = max(2, min(args.steps, 5))
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(iters):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / iters], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    rs = timed(lambda: dist.reduce_scatter_tensor(part, flat, op=dist.ReduceOp.AVG))
+    ag = timed(lambda: dist.all_gather_into_tensor(flat, part))
+    moved = 2 * (world - 1) / world * total * 2  # bytes each rank sends+receives per collective pair (ring model)
+    del flat, part
+    torch.cuda.empty_cache()
+    return {"reduce_scatter_ms": rs, "all_gather_ms": ag, "step_ms": step_ms,
+            "full_step_ms": rs + step_ms + ag, "params_padded": total,
+            "busbw_gbs": moved / ((rs + ag) * 1e-3) / 1e9,
+            "note": "NCCL over NVLink; bf16 grads reduce-scattered (AVG), bf16 params all-gathered in place"}
+
+
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -367,6 +411,13 @@ def run_ours(args) -> None:
         except Exception:
             traffic = None
 
+    zero1 = None
+    if world > 1 and not args.no_zero1:
+        try:
+            zero1 = zero1_exchange(sum(S.numel(s) for _, s in shapes), world, dev, stream, avg_kern_ms, args)
+        except Exception as ex:  # the headline line must still print
+            zero1 = {"error": f"{type(ex).__name__}: {ex}"[:200]}
+
     e2e = None
     cpu = None
     if rank == 0 and world == 1 and not args.no_e2e:
@@ -392,7 +443,7 @@ def run_ours(args) -> None:
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                          "bytes_per_param": bpp, "kernel_ms": avg_kern_ms,
                          "kernel": "fo::step_ws_kernel (cuda events on the launch stream)"},
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "zero1": zero1,
             "clocks": clk, "gpu_launches": args.steps * launches_per_step,
             "device_errors": emask,
         }
@@ -413,6 +464,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-zero1", action="store_true", help="N>1: skip the reduce-scatter/all-gather timing")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch (read+write), from profiles/, reported beside the roofline")
     ap.add_argument("--t0", type=int, default=1000,
