@@ -33,7 +33,7 @@ struct Luts6 {
 __device__ __forceinline__ void init_luts6(Luts6& L) {
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     const int rho = (int)(int8_t)i;
-    L.r[i] = rho == -128 ? 0 : __float2int_rn(__fmul_rn(__fdiv_rn((float)rho, 127.0f), 32768.0f));
+    L.r[i] = rho == -128 ? 0 : fast::recon_r(rho);
     L.m[i] = momentum_unit(rho);
     L.v[i] = variance_unit(i);
   }
@@ -251,13 +251,10 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const uint32_t w = hl[k & 3];
     const uint32_t rwd = hr[(j >> 2) & 1], mwd = hm[(j >> 2) & 1], vwd = hv[(j >> 2) & 1];
     // reconstruct (formats.py:248-276), see the header comment
-    // lp +- R as one IMAD: the direction is +1 for lp >= 0 and -1 for
-    // lp < 0 ((bits >> 30) | 1 with an arithmetic shift)
-    const uint32_t lpl = w << 16, lph = w & 0xFFFF0000u;
-    const int sl = ((int)lpl >> 30) | 1, sh = ((int)w >> 30) | 1;
+    // lp +- R as one IMAD (fast::recon_bits)
     const int rl = L.r[prmt(rwd, 0, 0x4440u + (j & 3))];
     const int rh = L.r[prmt(rwd, 0, 0x4440u + (j & 3) + 1)];
-    const float2 th2 = make_float2(__uint_as_float(lpl + (uint32_t)(rl * sl)), __uint_as_float(lph + (uint32_t)(rh * sh)));
+    const float2 th2 = make_float2(__uint_as_float(recon_bits(w << 16, rl)), __uint_as_float(recon_bits(w & 0xFFFF0000u, rh)));
     // dequantise (quantize.py:125-131, :152-158)
     const float2 u2 = make_float2(L.m[prmt(mwd, 0, 0x4440u + (j & 3))], L.m[prmt(mwd, 0, 0x4440u + (j & 3) + 1)]);
     const float2 mp2 = fma2(u2, dup(msf), Z);

@@ -53,3 +53,11 @@ def test_bias_correction_division_sampled(cuda_dev):
     """m/bc1, v/bc2 with host-side RN(1/bc), 2^30 samples of beta, t, a."""
     bad, first = _run(4, 0, 1 << 30)
     assert bad == 0, f"{bad} mismatches, first sample {first}"
+
+
+def test_integer_reconstruct_exhaustive(cuda_dev):
+    """The fused tile's integer reconstruct (fast::recon_bits + R(rho) LUT)
+    against the IEEE restatement for every finite bf16 code x every rho;
+    the two zero cases it gets wrong come out NaN or -0 (guard-tripping)."""
+    bad, first = _run(6, 0, 1 << 24)
+    assert bad == 0, f"{bad} mismatches, first at code {first >> 8:#06x} rho byte {first & 0xFF:#04x}"
