@@ -239,3 +239,51 @@ class TestErrors:
         fs = FO.init_flash_state(torch.ones(10, device=cuda_dev), "sgd")
         with pytest.raises(ValueError, match="length"):
             FO.sgd_step(fs, torch.ones(11, device=cuda_dev), FO.SgdHyperParams(lr=0.1))
+
+
+@pytest.mark.parametrize("opt", OPTS)
+def test_special_weight_codes(opt, cuda_dev, oracle_mod):
+    """Weight codes where the fused tile's shortcuts need their guards: +-0
+    with every correction sign (the integer reconstruct's two wrong cases),
+    subnormal codes, binade bottoms (the formats.py:147-154 refinement),
+    the largest finite bf16, and tiny gradients (|g| < 2^-35)."""
+    rng = np.random.default_rng(4242 + OPTS.index(opt))
+    special = np.array([0x0000, 0x8000, 0x0001, 0x8001, 0x007F, 0x0080, 0x8080, 0x0100, 0x8100, 0x3F80, 0xBF80,
+                        0x4000, 0xC000, 0x7F7F, 0xFF7F, 0x0700, 0x0701, 0x8700], np.uint16)
+    n = 16384 + 96
+    st = H.random_state(rng, n, opt)
+    lp = st["weights.lp"].copy()
+    pick = rng.random(n) < 0.25
+    lp[pick] = special[rng.integers(0, special.size, int(pick.sum()))]
+    st["weights.lp"] = lp
+    rho = st["weights.rho"]
+    rho[rng.random(n) < 0.05] = 0
+    g = H.random_grad(rng, n, std=1e-3)
+    tiny = rng.random(n) < 0.01
+    g[tiny] = (rng.standard_normal(int(tiny.sum())) * 2.0**-40).astype(np.float32)
+    g = H.bf16_round(g) if hasattr(H, "bf16_round") else g
+    mm = _run_pair(opt, st, g, 50, H.random_hparams(rng, opt), cuda_dev, oracle_mod)
+    assert all(v == 0 for v in mm.values()), mm
+
+
+@pytest.mark.parametrize("opt", ["adamw"])
+def test_more_tensors_than_one_launch(opt, cuda_dev, oracle_mod):
+    """> 384 tensors (FO_MT_MAX_TENSORS) in one call: several launches."""
+    from paper_2602_23349_b200 import optim as FO
+
+    rng = np.random.default_rng(99)
+    sizes = [int(x) for x in rng.integers(1, 3000, 450)] + [7680 * 3 + 517]
+    hp = H.random_hparams(rng, opt)
+    states, grads, refs = [], [], []
+    for n in sizes:
+        st = H.random_state(rng, n, opt)
+        g = H.random_grad(rng, n)
+        states.append(to_device(st, 700, cuda_dev))
+        grads.append(torch.from_numpy(g).to(cuda_dev).bfloat16())
+        ost = oracle_state(st, 700)
+        assert oracle_mod.step_inplace(opt, ost, g, **hp) == 0
+        refs.append(oracle_dict(ost))
+    FO.step_many(opt, states, grads, [_hp_obj(opt, hp)] * len(sizes))
+    for fs, ref in zip(states, refs):
+        mm = mismatches(from_device(fs), ref)
+        assert all(v == 0 for v in mm.values()), mm
