@@ -287,3 +287,19 @@ def test_more_tensors_than_one_launch(opt, cuda_dev, oracle_mod):
     for fs, ref in zip(states, refs):
         mm = mismatches(from_device(fs), ref)
         assert all(v == 0 for v in mm.values()), mm
+
+
+def test_ldg_kernel_matches_too(cuda_dev):
+    """The LDG kernel (taken when a list's scale runs are not 16-byte aligned,
+    FO_KERNEL=mt forces it) passes the same bitwise parity cases."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, FO_KERNEL="mt")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "fused_step_bitwise or multi_tensor or special or f32_gradients"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
