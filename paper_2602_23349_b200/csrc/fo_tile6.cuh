@@ -293,9 +293,12 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       tn2 = add2(th2, neg2(fma2(dup(h.lr), u, Z)));
     } else {
       const float2 c2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
-      float2 s2;  // np.sign with sign(+-0) = +0 (c is never -0 here)
-      s2.x = c2.x > 0.0f ? 1.0f : (c2.x < 0.0f ? -1.0f : (c2.x != c2.x ? c2.x : 0.0f));
-      s2.y = c2.y > 0.0f ? 1.0f : (c2.y < 0.0f ? -1.0f : (c2.y != c2.y ? c2.y : 0.0f));
+      // np.sign with sign(+-0) = +0: copysign(1, c), or +0 for c == 0.  A
+      // NaN c (non-finite input) makes m NaN too, which sends the tile to
+      // the exact path, so NaN need not propagate here.
+      const float2 s2 = make_float2(
+          __uint_as_float(c2.x == 0.0f ? 0u : ((__float_as_uint(c2.x) & 0x80000000u) | 0x3F800000u)),
+          __uint_as_float(c2.y == 0.0f ? 0u : ((__float_as_uint(c2.y) & 0x80000000u) | 0x3F800000u)));
       m2 = add2(fma2(dup(h.b2), mp2, Z), fma2(dup(h.omb2), g2, Z));
       const float2 u = add2(s2, fma2(dup(h.wd), th2, Z));
       tn2 = add2(th2, neg2(fma2(dup(h.lr), u, Z)));
