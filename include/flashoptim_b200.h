@@ -163,10 +163,21 @@ int fo_dequantize_variance(const uint8_t *codes, const uint16_t *scales, int64_t
  * intrinsics (no reference counterpart; test support).  mode 0: sqrt over
  * f32 bit patterns [begin, begin+count); 1: reciprocal of every fp16 value;
  * 2/3/4: hash-sampled quotients (per-element, per-group-scale and
- * bias-correction divisors).  d_out[0] += mismatches, d_out[1] = min failing
+ * bias-correction divisors); 6: the fused tile's integer reconstruct over
+ * every (bf16 code, rho).  d_out[0] += mismatches, d_out[1] = min failing
  * index (initialise to 0 and UINT64_MAX); mode 5 writes raw sqrt results to
  * d_out[2..] (debug). */
 int fo_selftest(int mode, uint64_t begin, uint64_t count, uint64_t *d_out, void *stream);
+
+/* Exhaustive FP32 reconstruction sweep (replaces sweep.py:166-218
+ * _sweep_block / :231 exhaustive_sweep_multi for the BF16 format).  Sweeps
+ * the (sign, exponent-field) blocks [block0, block0 + nblocks) of the 510
+ * finite ones; scheme_mask bit s selects sweep.SCHEMES[s] (ulp8, ulp16,
+ * none, baseline).  d_out: nblocks * 4 records of 8 uint64 each, zeroed by
+ * the caller: {count, exact, overflow, zero, zero_exact, (double) relsum,
+ * (float bits) relmax, unused}, the per-block tuple _sweep_block returns. */
+#define FO_SWEEP_RECORD_U64 8
+int fo_sweep(int block0, int nblocks, uint32_t scheme_mask, uint64_t *d_out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -73,6 +73,7 @@ SIGNATURES = {
     "fo_quantize_variance": (ctypes.c_int, [_P, _I64, _I32, _P, _P, _P, _P]),
     "fo_dequantize_variance": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
     "fo_selftest": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, _P, _P]),
+    "fo_sweep": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_uint32, _P, _P]),
     "fo_step_host": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(fo_tensor), _I32, ctypes.POINTER(fo_hparams), _I32,
                                     ctypes.c_int, ctypes.c_int, _I32, ctypes.c_int, _I64, ctypes.POINTER(_U32)]),
     "fo_host_release": (None, []),

@@ -180,4 +180,8 @@ int fo_selftest(int mode, uint64_t begin, uint64_t count, uint64_t* d_out, void*
   return fo::selftest(mode, begin, count, reinterpret_cast<unsigned long long*>(d_out), as_stream(stream));
 }
 
+int fo_sweep(int block0, int nblocks, uint32_t scheme_mask, uint64_t* d_out, void* stream) {
+  return fo::sweep(block0, nblocks, scheme_mask, d_out, as_stream(stream));
+}
+
 }  // extern "C"

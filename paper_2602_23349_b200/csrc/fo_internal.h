@@ -25,6 +25,7 @@ int step_host(int opt, const fo_tensor* ts, int32_t nt, const fo_hparams* hps, i
               int rho_bits, int32_t G, int var_scheme, int64_t chunk_elems, uint32_t* h_err);
 void host_release();
 int selftest(int mode, uint64_t begin, uint64_t count, unsigned long long* d_out, cudaStream_t s);
+int sweep(int block0, int nblocks, uint32_t scheme_mask, void* out, cudaStream_t s);
 int dequantize(bool variance, const void* codes, const uint16_t* scales, int64_t n, int64_t G, float* out,
                cudaStream_t s);
 
