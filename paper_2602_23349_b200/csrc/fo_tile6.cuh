@@ -45,6 +45,58 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
+// Compact LUTs (3 KB): index = code byte, one PRMT + one LEA per lookup.
+struct NarrowLut {
+  const Luts6& L;
+  __device__ __forceinline__ int r(uint32_t w, int j) const { return L.r[prmt(w, 0, 0x4440u + j)]; }
+  __device__ __forceinline__ float m(uint32_t w, int j) const { return L.m[prmt(w, 0, 0x4440u + j)]; }
+  __device__ __forceinline__ float v(uint32_t w, int j) const { return L.v[prmt(w, 0, 0x4440u + j)]; }
+};
+
+// Wide LUTs (64 KB at shared-window address 0x20000): row b (256 bytes)
+// holds 21 copies of each table, so the shared address
+// 0x20000 + 256*b + 4*(21*t + lane%21) is ONE PRMT of the code word with a
+// per-lane register holding 0x00020000 | offset (code byte -> byte 1,
+// offset -> byte 0, 0x02 -> byte 2): no address arithmetic at all, and the
+// lanes of a warp hit distinct banks except l and l+21 (at most 2-way
+// conflicts, against ~3.5-way for random indices into a compact table).
+constexpr int WIDE_COPIES = 21;
+constexpr uint32_t WIDE_LUT_ADDR = 0x20000u;
+constexpr uint32_t WIDE_LUT_BYTES = 256u * 256u;
+struct WideLut {
+  uint32_t o_r, o_m, o_v;  // 0x20000 | 4*(21*t + lane%21), t = 0, 1, 2
+  __device__ __forceinline__ static uint32_t ld(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+  }
+  __device__ __forceinline__ int r(uint32_t w, int j) const { return (int)ld(prmt(w, o_r, 0x7604u | ((uint32_t)j << 4))); }
+  __device__ __forceinline__ float m(uint32_t w, int j) const {
+    return __uint_as_float(ld(prmt(w, o_m, 0x7604u | ((uint32_t)j << 4))));
+  }
+  __device__ __forceinline__ float v(uint32_t w, int j) const {
+    return __uint_as_float(ld(prmt(w, o_v, 0x7604u | ((uint32_t)j << 4))));
+  }
+};
+
+// `dsm`: the CTA's dynamic shared memory, at least WIDE_LUT_ADDR +
+// WIDE_LUT_BYTES - (its shared address) bytes long.
+__device__ __forceinline__ WideLut init_wide_lut(uint8_t* dsm) {
+  uint8_t* base = dsm + (WIDE_LUT_ADDR - (uint32_t)__cvta_generic_to_shared(dsm));
+  for (int i = threadIdx.x; i < 256 * 3 * WIDE_COPIES; i += blockDim.x) {
+    const int b = i / (3 * WIDE_COPIES), w = i % (3 * WIDE_COPIES), t = w / WIDE_COPIES;
+    const int code = (int)(int8_t)b;
+    uint32_t val;
+    if (t == 0) val = (uint32_t)(code == -128 ? 0 : fast::recon_r(code));
+    else if (t == 1) val = __float_as_uint(momentum_unit(code));
+    else val = __float_as_uint(variance_unit(b));
+    reinterpret_cast<uint32_t*>(base + b * 256)[w] = val;
+  }
+  const uint32_t c = (threadIdx.x & 31) % WIDE_COPIES;
+  return WideLut{WIDE_LUT_ADDR | (4u * c), WIDE_LUT_ADDR | (4u * (WIDE_COPIES + c)),
+                 WIDE_LUT_ADDR | (4u * (2 * WIDE_COPIES + c))};
+}
+
 // The exact recompute is rare (guards only trip on magnitudes training does
 // not produce); keeping it out of line keeps its register demand out of the
 // fast path's allocation.
@@ -174,9 +226,9 @@ struct RegSrc {  // a partial tile already gathered into registers
   }
 };
 
-template <int OPT, typename GradT, int BC, class Src>
+template <int OPT, typename GradT, int BC, class Src, class Lut>
 __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h, int64_t base, int lane,
-                                              uint32_t& err, const Luts6& L, float negzero, uint32_t* err_out,
+                                              uint32_t& err, const Lut& L, float negzero, uint32_t* err_out,
                                               bool full, const Src& in) {
   using namespace fast;
   constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
@@ -252,11 +304,11 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const uint32_t rwd = hr[(j >> 2) & 1], mwd = hm[(j >> 2) & 1], vwd = hv[(j >> 2) & 1];
     // reconstruct (formats.py:248-276), see the header comment
     // lp +- R as one IMAD (fast::recon_bits)
-    const int rl = L.r[prmt(rwd, 0, 0x4440u + (j & 3))];
-    const int rh = L.r[prmt(rwd, 0, 0x4440u + (j & 3) + 1)];
+    const int rl = L.r(rwd, j & 3);
+    const int rh = L.r(rwd, (j & 3) + 1);
     const float2 th2 = make_float2(__uint_as_float(recon_bits(w << 16, rl)), __uint_as_float(recon_bits(w & 0xFFFF0000u, rh)));
     // dequantise (quantize.py:125-131, :152-158)
-    const float2 u2 = make_float2(L.m[prmt(mwd, 0, 0x4440u + (j & 3))], L.m[prmt(mwd, 0, 0x4440u + (j & 3) + 1)]);
+    const float2 u2 = make_float2(L.m(mwd, j & 3), L.m(mwd, (j & 3) + 1));
     const float2 mp2 = fma2(u2, dup(msf), Z);
     float2 g2;
     if (sizeof(GradT) == 2) {
@@ -268,7 +320,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     // update (optim.py:393-396, :418-424, :445-447)
     float2 m2, tn2;
     if (OPT == FO_OPT_ADAMW) {
-      const float2 z2 = make_float2(L.v[prmt(vwd, 0, 0x4440u + (j & 3))], L.v[prmt(vwd, 0, 0x4440u + (j & 3) + 1)]);
+      const float2 z2 = make_float2(L.v(vwd, j & 3), L.v(vwd, (j & 3) + 1));
       const float2 r2 = fma2(z2, dup(vsf), Z);
       const float2 vp2 = fma2(r2, r2, Z);
       m2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
