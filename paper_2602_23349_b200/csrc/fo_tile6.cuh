@@ -186,6 +186,7 @@ struct SmemSrc {  // a full tile in the stage ring (read in place)
   static constexpr int NGH = TileIn6<GradT>::NG / 2;
   const uint8_t *lp, *g, *rho, *mq, *vq;
   uint32_t msb, vsb;
+  uint32_t release_bar;  // mbarrier to arrive on once the second half is read (0: none)
   __device__ __forceinline__ void half(int h, uint32_t* lw, uint32_t* gw, uint32_t* rw, uint32_t* mw,
                                        uint32_t* vw) const {
     const uint4 a = *reinterpret_cast<const uint4*>(lp + 16 * h);
@@ -202,6 +203,13 @@ struct SmemSrc {  // a full tile in the stage ring (read in place)
     if (OPT == FO_OPT_ADAMW) {
       const uint2 v = *reinterpret_cast<const uint2*>(vq + 8 * h);
       vw[0] = v.x; vw[1] = v.y;
+    }
+    if (h == 1 && release_bar) {
+      // the warp's last reads of this stage are issued: release it now (the
+      // arrive's release semantics order the reads before the producer's
+      // next bulk copy into the stage), half a tile before the compute ends
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(release_bar) : "memory");
     }
   }
 };
