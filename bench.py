@@ -327,10 +327,26 @@ def run_ours(args) -> None:
     from paper_2602_23349_b200.optim import HP_TYPES
 
     rank, world, local = dist_env()
+    # FO_BENCH_DIST_BACKEND=gloo is a test mode for the N > 1 code path on a
+    # box with fewer GPUs than ranks (ranks share devices, reductions go
+    # through host copies, the NCCL exchange is skipped); timings from it are
+    # not the product's.
+    backend = os.environ.get("FO_BENCH_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+
+    def reduce_(t, op):
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+        return t
     opt = args.optimizer
     shapes = S.CONFIGS[args.config]()
     sizes = [S.numel(s) for _, s in shapes]
@@ -389,10 +405,10 @@ def run_ours(args) -> None:
     avg_kern_ms = sum(kern_ms) / len(kern_ms)
     if world > 1:
         tt = torch.tensor([total_ms, avg_kern_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        reduce_(tt, dist.ReduceOp.MAX)
         total_ms, avg_kern_ms = float(tt[0]), float(tt[1])
         nn = torch.tensor([n_local], device=dev, dtype=torch.float64)
-        dist.all_reduce(nn)
+        reduce_(nn, dist.ReduceOp.SUM)
         n_all = int(nn.item())
     else:
         n_all = n_local
@@ -412,7 +428,7 @@ def run_ours(args) -> None:
             traffic = None
 
     zero1 = None
-    if world > 1 and not args.no_zero1:
+    if world > 1 and not args.no_zero1 and backend == "nccl":
         try:
             zero1 = zero1_exchange(sum(S.numel(s) for _, s in shapes), world, dev, stream, avg_kern_ms, args)
         except Exception as ex:  # the headline line must still print
@@ -420,9 +436,33 @@ def run_ours(args) -> None:
 
     e2e = None
     cpu = None
-    if rank == 0 and world == 1 and not args.no_e2e:
-        e2e = host_e2e(fl, grads_flat, opt, hp, args.t0 + args.warmup + args.steps,
-                       steps=min(args.steps, args.e2e_steps), warmup=1)
+    if not args.no_e2e:
+        # every rank streams its own shard through fo_step_host (its own
+        # PCIe link); value = all params / slowest rank's time.  Skipped when
+        # the host cannot pin all shards' state (the whole list needs ~12.25
+        # bytes/param of pinned memory across ranks).
+        need = n_local * BYTES_PER_PARAM[opt] * 1.15
+        try:
+            import psutil
+
+            avail = psutil.virtual_memory().available / max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+        except Exception:
+            avail = float("inf")
+        if avail < need:
+            e2e = {"skipped": f"host memory: {avail / 1e9:.0f} GB available per rank, {need / 1e9:.0f} GB needed"}
+        else:
+            if world > 1:
+                dist.barrier()
+            e2e = host_e2e(fl, grads_flat, opt, hp, args.t0 + args.warmup + args.steps,
+                           steps=min(args.steps, args.e2e_steps), warmup=1)
+            if world > 1:
+                tt = torch.tensor([e2e["ms_per_step"], e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]],
+                                  device=dev, dtype=torch.float64)
+                reduce_(tt[:1], dist.ReduceOp.MAX)
+                reduce_(tt[1:], dist.ReduceOp.SUM)
+                e2e.update({"ms_per_step": float(tt[0]), "h2d_bytes_per_step": int(tt[1]),
+                            "d2h_bytes_per_step": int(tt[2]), "value": n_all / (float(tt[0]) * 1e-3) / 1e9,
+                            "ranks": world})
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample_run(opt, args.config, args.ref_seconds, len(os.sched_getaffinity(0)))
     if rank == 0:
