@@ -418,7 +418,7 @@ def run_ours(args) -> None:
     peak, peak_kind = peaks()
     bpp = BYTES_PER_PARAM[opt]
     achieved = n_local * bpp / (avg_kern_ms * 1e-3) / 1e9
-    launches_per_step = (len(sizes) + 383) // 384  # one hyper-parameter set, <= 384 tensors per launch
+    launches_per_step = 2 * ((len(sizes) + 383) // 384)  # fused step + fix-up per <= 384 tensors
     traffic = args.traffic
     if traffic is None:
         try:

@@ -97,15 +97,6 @@ __device__ __forceinline__ WideLut init_wide_lut(uint8_t* dsm) {
                  WIDE_LUT_ADDR | (4u * (2 * WIDE_COPIES + c))};
 }
 
-// The exact recompute is rare (guards only trip on magnitudes training does
-// not produce); keeping it out of line keeps its register demand out of the
-// fast path's allocation.
-template <int OPT, typename GradT>
-__device__ __noinline__ void exact_tile_call(const TArg T, const fo_hparams h, int64_t base, int lane,
-                                             uint32_t* err_out) {
-  process_tile_exact<OPT, GradT, FEPL>(T, h, base, lane, err_out);
-}
-
 template <typename GradT>
 struct TileIn6 {
   static constexpr int E = FEPL, NW = FEPL / 2, NB = FEPL / 4;
@@ -234,10 +225,15 @@ struct RegSrc {  // a partial tile already gathered into registers
   }
 };
 
+// A tripped guard does not recompute in place: lane 0 sets bit `fix_idx` of
+// `fix` and the tile stores nothing, so its inputs stay intact in global
+// memory for the fix-up launch that follows every fused launch
+// (step_fixup_kernel: process_tile_exact on the flagged slices, which also
+// sets the reference's error bits).  The fast kernel carries no fallback code.
 template <int OPT, typename GradT, int BC, class Src, class Lut>
 __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h, int64_t base, int lane,
-                                              uint32_t& err, const Lut& L, float negzero, uint32_t* err_out,
-                                              bool full, const Src& in) {
+                                              uint32_t& err, const Lut& L, float negzero, uint32_t* fix,
+                                              uint32_t fix_idx, bool full, const Src& in) {
   using namespace fast;
   constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
   constexpr int E = FEPL, NW = E / 2, NB = E / 4, LPG = GROUP / E;
@@ -443,7 +439,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 
   // ---- any guard tripped anywhere in the warp: recompute the tile exactly ----
   if (__any_sync(0xffffffffu, bad)) {
-    exact_tile_call<OPT, GradT>(T, h, base, lane, err_out);
+    if (lane == 0) atomicOr(fix + (fix_idx >> 5), 1u << (fix_idx & 31));
     return;
   }
 
