@@ -53,6 +53,13 @@ struct NarrowLut {
   __device__ __forceinline__ float v(uint32_t w, int j) const { return L.v[prmt(w, 0, 0x4440u + j)]; }
 };
 
+// No table: the SAFE re-run computes the dequantisation units directly.
+struct NoLut {
+  __device__ __forceinline__ int r(uint32_t w, int j) const { return fast::recon_r((int)(int8_t)(w >> (8 * j))); }
+  __device__ __forceinline__ float m(uint32_t w, int j) const { return momentum_unit((int)(int8_t)(w >> (8 * j))); }
+  __device__ __forceinline__ float v(uint32_t w, int j) const { return variance_unit((int)((w >> (8 * j)) & 0xFFu)); }
+};
+
 // Wide LUTs (64 KB at shared-window address 0x20000): row b (256 bytes)
 // holds 21 copies of each table, so the shared address
 // 0x20000 + 256*b + 4*(21*t + lane%21) is ONE PRMT of the code word with a
@@ -230,7 +237,28 @@ struct RegSrc {  // a partial tile already gathered into registers
 // memory for the fix-up launch that follows every fused launch
 // (step_fixup_kernel: process_tile_exact on the flagged slices, which also
 // sets the reference's error bits).  The fast kernel carries no fallback code.
-template <int OPT, typename GradT, int BC, class Src, class Lut>
+// Primitives of the fast tile and their IEEE forms (SAFE re-run, fix-up launch).
+template <bool SAFE>
+__device__ __forceinline__ float2 quot_y(float2 a, float b, float y) {  // a / b, y = RN(1/b)
+  if (SAFE) return make_float2(__fdiv_rn(a.x, b), __fdiv_rn(a.y, b));
+  return fast::div_y(a, fast::dup(b), fast::dup(y));
+}
+template <bool SAFE>
+__device__ __forceinline__ float2 quot(float2 a, float2 b) {
+  if (SAFE) return make_float2(__fdiv_rn(a.x, b.x), __fdiv_rn(a.y, b.y));
+  return fast::div_rn2(a, b);
+}
+template <bool SAFE>
+__device__ __forceinline__ float2 root2(float2 x) {
+  if (SAFE) return make_float2(__fsqrt_rn(x.x), __fsqrt_rn(x.y));
+  return fast::sqrt_rn2(x);
+}
+
+// SAFE = true (the fix-up launch only): the same tile with IEEE division /
+// square root and the exact reconstruct / split of fo_math.cuh, so only the
+// reference's error conditions (non-finite values, rho = -128, scale
+// overflow) remain; those go to process_tile_exact, which reports them.
+template <int OPT, typename GradT, int BC, class Src, class Lut, bool SAFE = false>
 __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h, int64_t base, int lane,
                                               uint32_t& err, const Lut& L, float negzero, uint32_t* fix,
                                               uint32_t fix_idx, bool full, const Src& in) {
@@ -273,7 +301,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   // (formats.py:270-271): as signed 16-bit lanes, a word whose high byte is
   // 0x80 is below -32512, and the shifted copy covers the low bytes.
   bool bad = false;
-  uint32_t gmin = 0xFFFFFFFFu, rmin = 0x7FFF7FFFu;
+  uint32_t gmin = 0xFFFFFFFFu, rmin = 0x7FFF7FFFu, gnf = 0;
   // A non-finite input scale makes every dequantised value of its group
   // non-finite (quantize.py:131,157): exact path.
   bad |= (in.msb & 0x7C00u) == 0x7C00u;
@@ -294,7 +322,15 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const int j = 2 * k;
     if ((k & 3) == 0) {
       in.half(k >> 2, hl, hg, hr, hm, hv);
-      if (sizeof(GradT) == 2) {
+      if (SAFE) {  // only non-finite gradients matter here (optim.py:380-381)
+        if (sizeof(GradT) == 2) {
+#pragma unroll
+          for (int q = 0; q < NGH; ++q) gnf |= __vcmpeq2(hg[q] & 0x7F807F80u, 0x7F807F80u);
+        } else {
+#pragma unroll
+          for (int q = 0; q < NGH; ++q) gnf |= (hg[q] & 0x7F800000u) == 0x7F800000u;
+        }
+      } else if (sizeof(GradT) == 2) {
 #pragma unroll
         for (int q = 0; q < NGH; ++q) gmin = __vminu2(gmin, __vsub2(hg[q] & 0x7FFF7FFFu, 0x00010001u));
       } else {
@@ -308,9 +344,16 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const uint32_t rwd = hr[(j >> 2) & 1], mwd = hm[(j >> 2) & 1], vwd = hv[(j >> 2) & 1];
     // reconstruct (formats.py:248-276), see the header comment
     // lp +- R as one IMAD (fast::recon_bits)
-    const int rl = L.r(rwd, j & 3);
-    const int rh = L.r(rwd, (j & 3) + 1);
-    const float2 th2 = make_float2(__uint_as_float(recon_bits(w << 16, rl)), __uint_as_float(recon_bits(w & 0xFFFF0000u, rh)));
+    float2 th2;
+    if (SAFE) {  // formats.py:248-276 restated (fo_math.cuh)
+      const int ql = (int)(int8_t)(rwd >> (8 * (j & 3))), qh = (int)(int8_t)(rwd >> (8 * ((j & 3) + 1)));
+      th2 = make_float2(reconstruct1(w & 0xFFFFu, ql, __fdiv_rn((float)ql, 127.0f)),
+                        reconstruct1(w >> 16, qh, __fdiv_rn((float)qh, 127.0f)));
+    } else {
+      const int rl = L.r(rwd, j & 3);
+      const int rh = L.r(rwd, (j & 3) + 1);
+      th2 = make_float2(__uint_as_float(recon_bits(w << 16, rl)), __uint_as_float(recon_bits(w & 0xFFFF0000u, rh)));
+    }
     // dequantise (quantize.py:125-131, :152-158)
     const float2 u2 = make_float2(L.m(mwd, j & 3), L.m(mwd, (j & 3) + 1));
     const float2 mp2 = fma2(u2, dup(msf), Z);
@@ -329,19 +372,19 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       const float2 vp2 = fma2(r2, r2, Z);
       m2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
       const float2 v2 = add2(fma2(dup(h.b2), vp2, Z), fma2(dup(h.omb2), fma2(g2, g2, Z), Z));
-      const float2 mh = (BC & 1) ? m2 : div_y(m2, dup(h.bc1), dup(h.rbc1));
+      const float2 mh = (BC & 1) ? m2 : quot_y<SAFE>(m2, h.bc1, h.rbc1);
       float2 rt2;  // RN(sqrt(v)), also quantize.py:145
       float2 den;
       if (BC & 2) {
-        rt2 = sqrt_rn2(v2);
+        rt2 = root2<SAFE>(v2);
         den = add2(rt2, dup(h.eps));
       } else {
-        rt2 = sqrt_rn2(v2);
-        den = add2(sqrt_rn2(div_y(v2, dup(h.bc2), dup(h.rbc2))), dup(h.eps));
+        rt2 = root2<SAFE>(v2);
+        den = add2(root2<SAFE>(quot_y<SAFE>(v2, h.bc2, h.rbc2)), dup(h.eps));
       }
       root[j] = rt2.x;
       root[j + 1] = rt2.y;
-      const float2 u = add2(div_rn2(mh, den), fma2(dup(h.wd), th2, Z));
+      const float2 u = add2(quot<SAFE>(mh, den), fma2(dup(h.wd), th2, Z));
       tn2 = add2(th2, neg2(fma2(dup(h.lr), u, Z)));
     } else if (OPT == FO_OPT_SGD) {
       m2 = add2(fma2(dup(h.mu), mp2, Z), g2);
@@ -362,18 +405,28 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     m[j] = m2.x;
     m[j + 1] = m2.y;
     // split (formats.py:232-245)
-    __nv_bfloat162 c2 = __floats2bfloat162_rn(tn2.x, tn2.y);  // RNE, overflow -> inf
-    cw[k] = *reinterpret_cast<uint32_t*>(&c2);
-    const float2 lp2 = make_float2(__uint_as_float(cw[k] << 16), __uint_as_float(cw[k] & 0xFFFF0000u));
-    const float2 e2 = add2(tn2, neg2(lp2));  // exact residual
-    // K = 127 * 2^-ell with ell = expf(theta) - 135: the binade-bottom rule is
-    // implied by theta's own exponent; valid for expf(theta) in [14, 254].
-    const float2 k2 = make_float2(__uint_as_float(0x867E0000u - (__float_as_uint(tn2.x) & 0x7F800000u)),
-                                  __uint_as_float(0x867E0000u - (__float_as_uint(tn2.y) & 0x7F800000u)));
-    // e*K is exact (<= 24 significant bits), so adding 1.5*2^23 in the same
-    // FFMA2 leaves rint(e*K) (ties-to-even) in the low mantissa bits.
-    const float2 q2 = fma2(e2, k2, dup(12582912.0f));
-    const uint32_t pr = prmt(__float_as_uint(q2.x), __float_as_uint(q2.y), 0x0040u);  // two codes -> bytes 0, 1
+    uint32_t pr;  // the two correction codes in bytes 0, 1
+    if (SAFE) {
+      uint32_t cl, ch;
+      int ql, qh;
+      split1<127>(tn2.x, cl, ql);
+      split1<127>(tn2.y, ch, qh);
+      cw[k] = cl | (ch << 16);
+      pr = (uint32_t)(ql & 0xFF) | ((uint32_t)(qh & 0xFF) << 8);
+    } else {
+      __nv_bfloat162 c2 = __floats2bfloat162_rn(tn2.x, tn2.y);  // RNE, overflow -> inf
+      cw[k] = *reinterpret_cast<uint32_t*>(&c2);
+      const float2 lp2 = make_float2(__uint_as_float(cw[k] << 16), __uint_as_float(cw[k] & 0xFFFF0000u));
+      const float2 e2 = add2(tn2, neg2(lp2));  // exact residual
+      // K = 127 * 2^-ell with ell = expf(theta) - 135: the binade-bottom rule
+      // is implied by theta's own exponent; valid for expf(theta) in [14, 254].
+      const float2 k2 = make_float2(__uint_as_float(0x867E0000u - (__float_as_uint(tn2.x) & 0x7F800000u)),
+                                    __uint_as_float(0x867E0000u - (__float_as_uint(tn2.y) & 0x7F800000u)));
+      // e*K is exact (<= 24 significant bits), so adding 1.5*2^23 in the same
+      // FFMA2 leaves rint(e*K) (ties-to-even) in the low mantissa bits.
+      const float2 q2 = fma2(e2, k2, dup(12582912.0f));
+      pr = prmt(__float_as_uint(q2.x), __float_as_uint(q2.y), 0x0040u);
+    }
     if (k & 1) ro[k >> 1] = prmt(ro[k >> 1], pr, 0x5410u);
     else ro[k >> 1] = pr;
     tmin = fminf(tmin, fminf(fabsf(tn2.x), fabsf(tn2.y)));
@@ -382,9 +435,15 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   // |theta_new| in [2^-113, bf16 max): the split's exponent rule holds, and
   // the reconstruct's zero cases (NaN, or a zero whose sign may differ from
   // the reference's) are excluded.  NaN fails both comparisons.
-  bad |= !(tmin >= 0x1p-113f) || !(tmax < 0x1.FFp127f);
-  if (sizeof(GradT) == 2) bad |= __vcmpltu2(gmin, 0x2DFF2DFFu) != 0;
-  else bad |= gmin < (0x2E000000u * 2u - 1u);
+  if (SAFE) {
+    // only the reference's error conditions remain: a non-finite weight
+    // (split-nonfinite) or gradient (gradient-nonfinite)
+    bad |= !(tmax <= 3.4028235e38f) || gnf != 0;
+  } else {
+    bad |= !(tmin >= 0x1p-113f) || !(tmax < 0x1.FFp127f);
+    if (sizeof(GradT) == 2) bad |= __vcmpltu2(gmin, 0x2DFF2DFFu) != 0;
+    else bad |= gmin < (0x2E000000u * 2u - 1u);
+  }
   bad |= __vcmplts2(rmin, 0x81008100u) != 0;
 
   // ---- epilogue: momentum (quantize.py:109-122), exact ----
@@ -402,11 +461,11 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const float y = rcp_rn_normal(den);
 #pragma unroll
     for (int j = 0; j < E; j += 2) {
-      const float2 mn = div_y(make_float2(m[j], m[j + 1]), dup(den), dup(y));  // RN(m/s)
+      const float2 mn = quot_y<SAFE>(make_float2(m[j], m[j + 1]), den, y);  // RN(m/s)
       const float2 d = make_float2(__fadd_rn(1.0f, fabsf(mn.x)), __fadd_rn(1.0f, fabsf(mn.y)));
       // RN(2m'/(1+|m'|)) = 2*RN(m'/(1+|m'|)) (power-of-two scaling), so
       // RN(z*127) = RN(RN(m'/d)*254)
-      const float2 zh = div_rn2(mn, d);
+      const float2 zh = quot<SAFE>(mn, d);
       const float2 t = add2(fma2(zh, dup(254.0f), Z), dup(12582912.0f));  // rint(RN(z*127))
       const uint32_t pr = prmt(__float_as_uint(t.x), __float_as_uint(t.y), 0x0040u);
       if (j & 2) mo[j >> 2] = prmt(mo[j >> 2], pr, 0x5410u);
@@ -429,7 +488,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const float y = rcp_rn_normal(den);
 #pragma unroll
     for (int j = 0; j < E; j += 2) {
-      const float2 vn = div_y(make_float2(root[j], root[j + 1]), dup(den), dup(y));  // RN(r/s)
+      const float2 vn = quot_y<SAFE>(make_float2(root[j], root[j + 1]), den, y);  // RN(r/s)
       const float2 t = add2(fma2(vn, dup(255.0f), Z), dup(12582912.0f));           // rint(RN(vn*255))
       const uint32_t pr = prmt(__float_as_uint(t.x), __float_as_uint(t.y), 0x0040u);
       if (j & 2) vo[j >> 2] = prmt(vo[j >> 2], pr, 0x5410u);
@@ -439,7 +498,8 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 
   // ---- any guard tripped anywhere in the warp: recompute the tile exactly ----
   if (__any_sync(0xffffffffu, bad)) {
-    if (lane == 0) atomicOr(fix + (fix_idx >> 5), 1u << (fix_idx & 31));
+    if (SAFE) process_tile_exact<OPT, GradT, FEPL>(T, h, base, lane, fix);  // `fix` = error word here
+    else if (lane == 0) atomicOr(fix + (fix_idx >> 5), 1u << (fix_idx & 31));
     return;
   }
 
@@ -470,3 +530,40 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   (void)err;
 }
 
+// A full tile straight from global memory with 128-bit loads.
+template <int OPT, typename GradT>
+__device__ __forceinline__ void load6_global_full(const TArg& T, int64_t base, int lane, TileIn6<GradT>& in) {
+  constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
+  constexpr int E = FEPL, NG = TileIn6<GradT>::NG;
+  const int64_t e0 = base + (int64_t)lane * E;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const uint4 a = ldcs4(T.lp + e0 + 8 * c);
+    in.lw[4 * c] = a.x; in.lw[4 * c + 1] = a.y; in.lw[4 * c + 2] = a.z; in.lw[4 * c + 3] = a.w;
+  }
+#pragma unroll
+  for (int c = 0; c < NG / 4; ++c) {
+    const uint4 a = ldcs4(reinterpret_cast<const GradT*>(T.g) + e0 + (16 / sizeof(GradT)) * c);
+    in.gw[4 * c] = a.x; in.gw[4 * c + 1] = a.y; in.gw[4 * c + 2] = a.z; in.gw[4 * c + 3] = a.w;
+  }
+  load_bytes<4>(T.rho + e0, in.rw);
+  load_bytes<4>(T.mq + e0, in.mw);
+  if (ADAM) load_bytes<4>(T.vq + e0, in.vw);
+  in.msb = T.ms[e0 >> 5];
+  in.vsb = ADAM ? (uint32_t)T.vs[e0 >> 5] : 0u;
+}
+
+// One flagged slice in the fix-up launch: the SAFE tile (exact everywhere the
+// fast one needed guards), or the straight restatement for error cases.
+template <int OPT, typename GradT, int BC>
+__device__ __forceinline__ void safe_tile(const TArg& T, const fo_hparams& h, int64_t base, int lane, float negzero,
+                                          uint32_t* err_out) {
+  const bool full = (T.n - base) >= FTILE;
+  TileIn6<GradT> in;
+  if (full) load6_global_full<OPT, GradT>(T, base, lane, in);
+  else load6_global<OPT, GradT>(T, base, lane, in);
+  const RegSrc<GradT> src{in, in.msb, in.vsb};
+  uint32_t err = 0;
+  const NoLut L;
+  compute_tile6<OPT, GradT, BC, RegSrc<GradT>, NoLut, true>(T, h, base, lane, err, L, negzero, err_out, 0, full, src);
+}
