@@ -153,8 +153,12 @@ __device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int la
   constexpr int E = FEPL, NW = E / 2, NB = E / 4, NG = TileIn6<GradT>::NG;
   const int64_t n = T.n;
   const int64_t e0 = base + (int64_t)lane * E;
+  // elements past n: weight 1.0 (0x3F80), zero correction, codes, scales
+  // and gradient -- their m and v are 0 (no effect on a group maximum) and
+  // their updated weight stays near 1, so they trip no guard; they are
+  // never stored
 #pragma unroll
-  for (int q = 0; q < NW; ++q) in.lw[q] = 0;
+  for (int q = 0; q < NW; ++q) in.lw[q] = 0x3F803F80u;
 #pragma unroll
   for (int q = 0; q < NG; ++q) in.gw[q] = 0;
 #pragma unroll
@@ -163,7 +167,7 @@ __device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int la
   for (int j = 0; j < E; ++j) {
     const int64_t i = e0 + j;
     if (i < n) {
-      in.lw[j >> 1] |= (uint32_t)T.lp[i] << (16 * (j & 1));
+      in.lw[j >> 1] = (in.lw[j >> 1] & (0xFFFF0000u >> (16 * (j & 1)))) | ((uint32_t)T.lp[i] << (16 * (j & 1)));
       in.rw[j >> 2] |= (uint32_t)(uint8_t)T.rho[i] << (8 * (j & 3));
       in.mw[j >> 2] |= (uint32_t)(uint8_t)T.mq[i] << (8 * (j & 3));
       if (ADAM) in.vw[j >> 2] |= (uint32_t)T.vq[i] << (8 * (j & 3));
