@@ -34,8 +34,12 @@ class FlatStates:
     """Optimizer-owned state buffers for `sizes`, with FlashState views."""
 
     def __init__(self, sizes: Sequence[int], optimizer: str, device, group_size: int = 32,
-                 lp_views: Sequence[torch.Tensor] | None = None):
+                 lp_views: Sequence[torch.Tensor] | None = None, rho_bits: int = 8,
+                 variance_scheme: str = "companded"):
+        if rho_bits not in (8, 16) or variance_scheme not in ("companded", "linear"):
+            raise ValueError("rho_bits must be 8 or 16 and variance_scheme companded or linear")
         self.optimizer = optimizer
+        self.variance_scheme = variance_scheme
         self.sizes = [int(s) for s in sizes]
         self.spec = GroupSpec(group_size)
         self.offsets, self.goffsets = [], []
@@ -47,7 +51,7 @@ class FlatStates:
             goff += _round_up(self.spec.num_groups(n), ALIGN // 2)
         self.total, self.gtotal = off, goff
         dev = torch.device(device)
-        self.rho = torch.zeros(off, dtype=torch.int8, device=dev)
+        self.rho = torch.zeros(off, dtype=torch.int8 if rho_bits == 8 else torch.int16, device=dev)
         self.m_codes = torch.zeros(off, dtype=torch.int8, device=dev)
         self.m_scales = torch.zeros(goff, dtype=torch.float16, device=dev)
         adam = optimizer == "adamw"
@@ -65,8 +69,9 @@ class FlatStates:
             m = QuantizedState(self.m_codes[o:o + n], self.m_scales[go:go + ng], self.spec, "momentum")
             v = None
             if adam:
-                v = QuantizedState(self.v_codes[o:o + n], self.v_scales[go:go + ng], self.spec, "variance")
-            self.states.append(FlashState(w, m, v, 0))
+                kind = "variance" if variance_scheme == "companded" else "linear-unsigned"
+                v = QuantizedState(self.v_codes[o:o + n], self.v_scales[go:go + ng], self.spec, kind)
+            self.states.append(FlashState(w, m, v, 0, variance_scheme if adam else "companded"))
 
     @property
     def numel(self) -> int:
