@@ -225,6 +225,60 @@ def init_random_state(fl, grads_flat, seed: int):
             v.copy_(torch.randn(v.numel(), generator=gen, device=dev) * scale)
 
 
+def pcie_peaks(nbytes: int = 1 << 29, reps: int = 3) -> dict:
+    """Pinned host <-> HBM copy bandwidth on this box (the e2e leg's
+    roofline): H2D alone, D2H alone, both at once on two streams."""
+    import torch
+
+    h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(h2d, d2h):
+        cur = torch.cuda.current_stream()
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        if h2d:
+            with torch.cuda.stream(s1):
+                d_a.copy_(h_in, non_blocking=True)
+        if d2h:
+            with torch.cuda.stream(s2):
+                h_out.copy_(d_b, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
+    def timed(h2d, d2h):
+        run(h2d, d2h)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            run(h2d, d2h)
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps * 1e-3
+
+    out = {"h2d_gbs": nbytes / timed(True, False) / 1e9, "d2h_gbs": nbytes / timed(False, True) / 1e9,
+           "bidir_each_gbs": nbytes / timed(True, True) / 1e9}
+    del h_in, h_out, d_a, d_b
+    torch.cuda.empty_cache()
+    return out
+
+
+def pcie_bound_s(h2d_bytes: float, d2h_bytes: float, pk: dict) -> float:
+    """Least time to move both byte counts: both directions at the
+    concurrent rate until the smaller one is done, the rest alone."""
+    both = min(h2d_bytes, d2h_bytes)
+    t = both / (pk["bidir_each_gbs"] * 1e9)
+    if h2d_bytes > d2h_bytes:
+        t += (h2d_bytes - both) / (pk["h2d_gbs"] * 1e9)
+    else:
+        t += (d2h_bytes - both) / (pk["d2h_gbs"] * 1e9)
+    return t
+
+
 def host_e2e(fl, grads_flat, opt, hp, t0, steps, warmup):
     """e2e: the same step through the C-ABI host-buffer entry point
     (fo_step_host): state + gradient in pinned host memory, H2D copy, fused
@@ -268,8 +322,11 @@ def host_e2e(fl, grads_flat, opt, hp, t0, steps, warmup):
         step_host(opt, states, grads, hp, chunk_elems=1 << 26, check=False)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t) / steps
+    pk = pcie_peaks()
+    bound = pcie_bound_s(h2d, d2h, pk)
     return {"value": sum(fl.sizes) / dt / 1e9, "unit": "Gparams/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3, "steps": steps, "warmup": warmup,
+            "roofline": {"bound": "pcie", "bound_ms": bound * 1e3, "frac": bound / dt, "pcie_measured": pk},
             "path": "fo_step_host (C ABI), pinned host buffers, 3 x 64M-element device slots",
             "host_setup_s": round(alloc_s, 1)}
 
@@ -463,6 +520,8 @@ def run_ours(args) -> None:
                 e2e.update({"ms_per_step": float(tt[0]), "h2d_bytes_per_step": int(tt[1]),
                             "d2h_bytes_per_step": int(tt[2]), "value": n_all / (float(tt[0]) * 1e-3) / 1e9,
                             "ranks": world})
+                # each rank streams over its own PCIe link: rank 0's bound vs the slowest rank
+                e2e["roofline"]["frac"] = e2e["roofline"]["bound_ms"] / e2e["ms_per_step"]
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_sample_run(opt, args.config, args.ref_seconds, len(os.sched_getaffinity(0)))
     if rank == 0:
@@ -474,7 +533,7 @@ def run_ours(args) -> None:
             "config": {"workload": f"{args.config} Flash{opt} fused step (state resident in HBM)",
                        "optimizer": opt, "params": n_all, "tensors": len(shapes),
                        "hbm_gbs_equiv": value * bpp, "step_t": args.t0 + 1,
-                       "l2": "working set >> 126 MB L2, no flush needed" if n_local * bpp > 1e9
+                       "l2": "working set >> 126 MB L2, no flush needed" if n_local * bpp > 2 * 126e6
                        else "L2-resident working set",
                        "parallelism": f"zero1-shard{world}" if world > 1 else "single-gpu"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
