@@ -87,16 +87,17 @@ struct WideLut {
 };
 
 // `dsm`: the CTA's dynamic shared memory, at least WIDE_LUT_ADDR +
-// WIDE_LUT_BYTES - (its shared address) bytes long.
-__device__ __forceinline__ WideLut init_wide_lut(uint8_t* dsm) {
+// WIDE_LUT_BYTES - (its shared address) bytes long.  The 768 distinct
+// values are computed once into `Ls` (the narrow tables) and then
+// replicated, so the prologue costs a few hundred stores per thread
+// instead of ~30 IEEE quotients.  Contains a __syncthreads.
+__device__ __forceinline__ WideLut init_wide_lut(uint8_t* dsm, Luts6& Ls) {
   uint8_t* base = dsm + (WIDE_LUT_ADDR - (uint32_t)__cvta_generic_to_shared(dsm));
+  init_luts6(Ls);
+  __syncthreads();
   for (int i = threadIdx.x; i < 256 * 3 * WIDE_COPIES; i += blockDim.x) {
     const int b = i / (3 * WIDE_COPIES), w = i % (3 * WIDE_COPIES), t = w / WIDE_COPIES;
-    const int code = (int)(int8_t)b;
-    uint32_t val;
-    if (t == 0) val = (uint32_t)(code == -128 ? 0 : fast::recon_r(code));
-    else if (t == 1) val = __float_as_uint(momentum_unit(code));
-    else val = __float_as_uint(variance_unit(b));
+    const uint32_t val = t == 0 ? (uint32_t)Ls.r[b] : __float_as_uint(t == 1 ? Ls.m[b] : Ls.v[b]);
     reinterpret_cast<uint32_t*>(base + b * 256)[w] = val;
   }
   const uint32_t c = (threadIdx.x & 31) % WIDE_COPIES;
