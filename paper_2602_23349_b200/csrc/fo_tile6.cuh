@@ -24,6 +24,10 @@
 #pragma once
 // (textually included inside namespace fo)
 
+#ifndef FO_VG
+#define FO_VG 1
+#endif
+
 struct Luts6 {
   int r[256];    // R(rho) by byte, signed; 0 for the invalid code -128 (caught by the rho guard)
   float m[256];  // quantize.py:129-130, z/(2-|z|) for every int8 code (by byte)
@@ -301,12 +305,19 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 #endif
 
   // ---- input guards (accumulated over the packed inputs in the loop) ----
-  // gradients: 0 < |g| < 2^-35 (the fast divisions / square roots rely on
-  // every nonzero m, v being far from the underflow range); rho == -128
+  // The fast divisions / square roots need their operands away from the
+  // underflow range.  FO_VG (default): guard the operands themselves --
+  // AdamW: every nonzero |m| >= 2^-84 and v >= 2^-94;
+  // SGD / Lion divide m only to quantise it, where a tiny m gives code 0
+  // either way, so they need no guard.  FO_VG=0: the older, stronger
+  // condition on the inputs, 0 < |g| < 2^-35 trips.  rho == -128
   // (formats.py:270-271): as signed 16-bit lanes, a word whose high byte is
   // 0x80 is below -32512, and the shifted copy covers the low bytes.
+  constexpr bool VG = FO_VG != 0;
   bool bad = false;
   uint32_t gmin = 0xFFFFFFFFu, rmin = 0x7FFF7FFFu, gnf = 0;
+  // min over 2 * (bits of |m|, v) - 2: the sign bit shifts out, +-0 maps to the top
+  uint32_t mlo = 0xFFFFFFFFu, vlo = 0xFFFFFFFFu;
   // A non-finite input scale makes every dequantised value of its group
   // non-finite (quantize.py:131,157): exact path.
   bad |= (in.msb & 0x7C00u) == 0x7C00u;
@@ -335,6 +346,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 #pragma unroll
           for (int q = 0; q < NGH; ++q) gnf |= (hg[q] & 0x7F800000u) == 0x7F800000u;
         }
+      } else if (VG) {
       } else if (sizeof(GradT) == 2) {
 #pragma unroll
         for (int q = 0; q < NGH; ++q) gmin = __vminu2(gmin, __vsub2(hg[q] & 0x7FFF7FFFu, 0x00010001u));
@@ -377,6 +389,10 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       const float2 vp2 = fma2(r2, r2, Z);
       m2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
       const float2 v2 = add2(fma2(dup(h.b2), vp2, Z), fma2(dup(h.omb2), fma2(g2, g2, Z), Z));
+      if (!SAFE && VG) {
+        mlo = __vimin3_u32(mlo, (__float_as_uint(m2.x) << 1) - 2u, (__float_as_uint(m2.y) << 1) - 2u);
+        vlo = __vimin3_u32(vlo, (__float_as_uint(v2.x) << 1) - 2u, (__float_as_uint(v2.y) << 1) - 2u);
+      }
       const float2 mh = (BC & 1) ? m2 : quot_y<SAFE>(m2, h.bc1, h.rbc1);
       float2 rt2;  // RN(sqrt(v)), also quantize.py:145
       float2 den;
@@ -446,8 +462,13 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     bad |= !(tmax <= 3.4028235e38f) || gnf != 0;
   } else {
     bad |= !(tmin >= 0x1p-113f) || !(tmax < 0x1.FFp127f);
-    if (sizeof(GradT) == 2) bad |= __vcmpltu2(gmin, 0x2DFF2DFFu) != 0;
-    else bad |= gmin < (0x2E000000u * 2u - 1u);
+    if (VG) {
+      if (ADAM) bad |= mlo < 2u * 0x15800000u - 2u || vlo < 2u * 0x10800000u - 2u;  // 0 < |m| < 2^-84, 0 < v < 2^-94
+    } else if (sizeof(GradT) == 2) {
+      bad |= __vcmpltu2(gmin, 0x2DFF2DFFu) != 0;
+    } else {
+      bad |= gmin < (0x2E000000u * 2u - 1u);
+    }
   }
   bad |= __vcmplts2(rmin, 0x81008100u) != 0;
 

@@ -303,3 +303,30 @@ def test_ldg_kernel_matches_too(cuda_dev):
                         "fused_step_bitwise or multi_tensor or special or f32_gradients"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("opt", OPTS)
+@pytest.mark.parametrize("case", ["live_state", "zero_state", "subnormal"])
+def test_tiny_gradients(opt, case, cuda_dev, oracle_mod):
+    """Gradients far below the typical scale (real bf16 backward passes have
+    them): on a live state the fast tile takes them (its guards look at the
+    m / v operands, not at g); from the zero state m and v are tiny too and
+    the guards must send the slices to the exact re-run.  Bitwise."""
+    rng = np.random.default_rng(9000 + 10 * OPTS.index(opt) + ["live_state", "zero_state", "subnormal"].index(case))
+    n = 65536 + 1000
+    st = H.random_state(rng, n, opt)
+    t = 40
+    if case == "zero_state":
+        for k in st:
+            if k not in ("weights.lp", "weights.rho"):
+                st[k] = np.zeros_like(st[k])
+        t = 0
+    g = H.random_grad(rng, n, std=1e-3)
+    pick = rng.random(n) < 0.3
+    exps = rng.uniform(-60, -30, int(pick.sum())) if case != "subnormal" else rng.uniform(-149, -120, int(pick.sum()))
+    tiny = (np.sign(rng.standard_normal(int(pick.sum()))) * 2.0 ** exps).astype(np.float32)
+    g[pick] = tiny
+    g = (g.view(np.uint32) & 0xFFFF0000).view(np.float32)  # bf16-exact
+    hp = H.random_hparams(rng, opt)
+    mm = _run_pair(opt, st, g, t, hp, cuda_dev, oracle_mod)
+    assert all(v == 0 for v in mm.values()), mm

@@ -37,3 +37,12 @@ for every in (0, 1000, 100, 10, 1):
         p.grad = gg.view(p.shape)
     ms = timeit()
     print(f"tiny grad in every {every or 'no'} slice(s): {ms:.3f} ms  ({n / ms / 1e6:.1f} Gparams/s)")
+# clustered: the leading 1% / 10% of every tensor holds tiny gradients (like
+# embedding rows of tokens absent from the batch)
+for frac in (0.01, 0.1):
+    for p, gb in zip(ps, base):
+        gg = gb.clone().reshape(-1)
+        gg[:int(gg.numel() * frac)] = 1e-12
+        p.grad = gg.view(p.shape)
+    ms = timeit()
+    print(f"tiny grads in the leading {frac:.0%} of every tensor: {ms:.3f} ms  ({n / ms / 1e6:.1f} Gparams/s)")
