@@ -183,3 +183,63 @@ def test_pergroup_kernel_still_matches(cuda_dev):
                         os.path.join(here, "test_gpu_g32.py"), "-k", "int16 or linear or misaligned or outside"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("opt", OPTS)
+def test_int16_every_code(opt, cuda_dev, oracle_mod):
+    """Every valid int16 correction code once (the reconstruct's division by
+    32767 is a Markstein quotient on the fast variant)."""
+    rng = np.random.default_rng(190 + OPTS.index(opt))
+    n = 65535
+    st = H.random_state(rng, n, opt)
+    st["weights.rho"] = rng.permutation(np.arange(-32767, 32768)).astype(np.int16)
+    g = H.random_grad(rng, n)
+    hp = H.random_hparams(rng, opt)
+    from paper_2602_23349_b200 import optim as FO
+
+    fs = to_device(st, 7, cuda_dev)
+    FO.STEP_FUNCTIONS_INPLACE[opt](fs, torch.from_numpy(g).to(cuda_dev).bfloat16(), _hp_obj(opt, hp))
+    ost = oracle_state(st, 7)
+    assert oracle_mod.step_inplace(opt, ost, g, **hp) == 0
+    mm = mismatches(from_device(fs), oracle_dict(ost))
+    assert all(v == 0 for v in mm.values()), mm
+
+
+@pytest.mark.parametrize("opt", OPTS)
+def test_int16_tiny_gradients(opt, cuda_dev, oracle_mod):
+    """Tiny and subnormal gradients through the group-32 kernel's shortcuts
+    (per-element fallback to the IEEE intrinsics), live and zero state."""
+    rng = np.random.default_rng(195 + OPTS.index(opt))
+    for zero in (False, True):
+        n = 40000 + 17
+        st = _int16_state(rng, n, opt)
+        if zero:
+            for k in st:
+                if k not in ("weights.lp", "weights.rho"):
+                    st[k] = np.zeros_like(st[k])
+        g = H.random_grad(rng, n, std=1e-3)
+        pick = rng.random(n) < 0.3
+        g[pick] = (np.sign(rng.standard_normal(int(pick.sum()))) *
+                   2.0 ** rng.uniform(-149, -30, int(pick.sum()))).astype(np.float32)
+        g = (g.view(np.uint32) & 0xFFFF0000).view(np.float32)
+        hp = H.random_hparams(rng, opt)
+        from paper_2602_23349_b200 import optim as FO
+
+        t = 0 if zero else 30
+        fs = to_device(st, t, cuda_dev)
+        FO.STEP_FUNCTIONS_INPLACE[opt](fs, torch.from_numpy(g).to(cuda_dev).bfloat16(), _hp_obj(opt, hp))
+        ost = oracle_state(st, t)
+        assert oracle_mod.step_inplace(opt, ost, g, **hp) == 0
+        mm = mismatches(from_device(fs), oracle_dict(ost))
+        assert all(v == 0 for v in mm.values()), (zero, mm)
+
+
+def test_ieee_variant_still_matches(cuda_dev):
+    """FO_G32_FAST=0: the group-32 kernel on IEEE intrinsics throughout passes
+    the same parity cases."""
+    env = dict(os.environ, FO_G32_FAST="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_g32.py"), "-k", "int16 or linear or misaligned or outside"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
