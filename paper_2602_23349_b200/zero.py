@@ -151,3 +151,117 @@ class ZeroFlashOptimizer:
 
     def zero_grad(self) -> None:
         self.flat_grads.zero_()
+
+    # -- checkpoints (SURVEY.md §8e "sharded checkpoints") -----------------------
+    # A tensor's state can straddle ranks.  To keep the reference layout -- one
+    # FLOP v1 file per tensor with rank-1 (n,) records (checkpoint.py:73-80,
+    # :98-125) -- the shards are gathered in flat-buffer coordinates, each
+    # tensor's slices are cut out with the padding dropped, and rank 0 writes
+    # the files: byte-identical to what a single-GPU FlashState of the whole
+    # tensor writes.  Loading re-shards: every rank reads the files and keeps
+    # its own segments.
+
+    def _local_records(self) -> dict:
+        L = self.layout
+        dev = self.flat_params.device
+        adam = self.optimizer == "adamw"
+        rho_dt = self.states[0].weights.corrections.dtype if self.states else torch.int8
+        loc = {"rho": torch.zeros(L.shard, dtype=rho_dt, device=dev),
+               "mq": torch.zeros(L.shard, dtype=torch.int8, device=dev),
+               "ms": torch.zeros(L.shard // 32, dtype=torch.float16, device=dev)}
+        if adam:
+            loc["vq"] = torch.zeros(L.shard, dtype=torch.uint8, device=dev)
+            loc["vs"] = torch.zeros(L.shard // 32, dtype=torch.float16, device=dev)
+        for seg, st in zip(self.segments, self.states):
+            a, n, ga = seg.shard_off, seg.length, seg.shard_off // 32
+            loc["rho"][a:a + n].copy_(st.weights.corrections)
+            loc["mq"][a:a + n].copy_(st.momentum.codes)
+            loc["ms"][ga:ga + st.momentum.scales.numel()].copy_(st.momentum.scales)
+            if adam:
+                loc["vq"][a:a + n].copy_(st.variance.codes)
+                loc["vs"][ga:ga + st.variance.scales.numel()].copy_(st.variance.scales)
+        return loc
+
+    def _gather_records(self) -> dict:
+        """All ranks' state records in flat-buffer coordinates (collective)."""
+        out = {}
+        for k, t in self._local_records().items():
+            raw = t.view(torch.uint8)  # bytes: every backend gathers them, bit patterns untouched
+            parts = [torch.empty_like(raw) for _ in range(self.world)]
+            dist.all_gather(parts, raw, group=self.pg)
+            out[k] = torch.cat(parts).view(t.dtype)
+        return out
+
+    def save_checkpoint(self, directory, names: Sequence[str] | None = None) -> dict | None:
+        """Collective: one FLOP v1 file per parameter plus a manifest, written
+        by rank 0 (returns the manifest there, None elsewhere)."""
+        import json
+        import os
+
+        import numpy as np
+
+        from .checkpoint import save_checkpoint
+        from .host import HostFlashState
+
+        g = self._gather_records()
+        manifest = None
+        if self.rank == 0:
+            os.makedirs(directory, exist_ok=True)
+            L = self.layout
+            names = list(names) if names is not None else [f"param{i:05d}" for i in range(len(self.params))]
+            host = {k: v.cpu().numpy() for k, v in g.items()}
+            lp_all = self.flat_params.view(torch.int16).cpu().numpy().view(np.uint16)
+            manifest = {"format": "FLOP v1 per parameter", "optimizer": self.optimizer, "params": [], "bytes": 0}
+            for i, (p, o, n) in enumerate(zip(self.params, L.offsets, L.numels)):
+                go, ng = o // 32, -(-n // 32)
+                hs = HostFlashState(lp_all[o:o + n], host["rho"][o:o + n], host["mq"][o:o + n],
+                                    host["ms"][go:go + ng], host["vq"][o:o + n] if "vq" in host else None,
+                                    host["vs"][go:go + ng] if "vs" in host else None, self.t, 32)
+                fname = f"{i:05d}.flop"
+                manifest["bytes"] += save_checkpoint(hs, os.path.join(directory, fname), self.optimizer)
+                manifest["params"].append({"index": i, "name": names[i], "file": fname, "shape": list(p.shape)})
+            with open(os.path.join(directory, "manifest.json"), "w") as f:
+                json.dump(manifest, f, indent=1)
+        dist.barrier(group=self.pg)
+        return manifest
+
+    @torch.no_grad()
+    def load_checkpoint(self, directory) -> None:
+        """Restore the full bf16 parameters and this rank's state segments from
+        files written by save_checkpoint (or by single-GPU save_optimizer)."""
+        import json
+        import os
+
+        from .checkpoint import CheckpointError, load_checkpoint
+
+        with open(os.path.join(directory, "manifest.json")) as f:
+            manifest = json.load(f)
+        if manifest["optimizer"] != self.optimizer:
+            raise CheckpointError(f"checkpoint is for {manifest['optimizer']}, optimizer is {self.optimizer}")
+        if len(manifest["params"]) != len(self.params):
+            raise CheckpointError("parameter count differs from the checkpoint")
+        L = self.layout
+        dev = self.flat_params.device
+        by_param: dict = {}
+        for seg, st in zip(self.segments, self.states):
+            by_param.setdefault(seg.param_index, []).append((seg, st))
+        step = None
+        for i, ent in enumerate(manifest["params"]):
+            hs = load_checkpoint(os.path.join(directory, ent["file"]))
+            o, n = L.offsets[i], L.numels[i]
+            if hs.length != n:
+                raise CheckpointError(f"parameter {i}: checkpoint has {hs.length} elements, model {n}")
+            step = hs.t
+            self.flat_params[o:o + n].copy_(torch.from_numpy(hs.lp.view("int16")).to(dev).view(torch.bfloat16))
+            for seg, st in by_param.get(i, []):
+                a, m, ga = seg.tensor_off, seg.length, seg.tensor_off // 32
+                T = lambda x: torch.from_numpy(x).to(dev)  # noqa: E731
+                st.weights.corrections.copy_(T(hs.rho[a:a + m]))
+                st.momentum.codes.copy_(T(hs.m_codes[a:a + m]))
+                st.momentum.scales.copy_(T(hs.m_scales[ga:ga + st.momentum.scales.numel()]))
+                if self.optimizer == "adamw":
+                    st.variance.codes.copy_(T(hs.v_codes[a:a + m]))
+                    st.variance.scales.copy_(T(hs.v_scales[ga:ga + st.variance.scales.numel()]))
+                st.t = hs.t
+        if step is not None:
+            self.t = int(step)

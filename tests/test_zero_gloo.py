@@ -139,3 +139,86 @@ def test_zero1_matches_unsharded_oracle(opt, oracle_mod):
         runs.sort()
         assert sum(ln for _, ln in runs) == SIZES[pi]
         assert runs[0][0] == 0 and all(a + b == c for (a, b), (c, _) in zip(runs, runs[1:]))
+
+
+def _worker_ckpt(rank, world, port, opt, q, directory):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2602_23349_b200 import optim as FO
+    from paper_2602_23349_b200.zero import ZeroFlashOptimizer
+
+    hp = {"adamw": [FO.AdamHyperParams(lr=1e-3, beta2=0.95, weight_decay=0.1), FO.AdamHyperParams(lr=1e-3)],
+          "sgd": [FO.SgdHyperParams(lr=0.1, weight_decay=1e-4), FO.SgdHyperParams(lr=0.1)],
+          "lion": [FO.LionHyperParams(lr=1e-4, weight_decay=0.1), FO.LionHyperParams(lr=1e-4)]}[opt]
+    params = _init_params()
+    zo = ZeroFlashOptimizer(params, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum")
+    for s in range(STEPS):
+        zo.zero_grad()
+        if rank == 0:
+            for p, g in zip(params, _grads(s)):
+                p.grad.copy_(g)
+        zo.step()
+    zo.save_checkpoint(directory)
+    # restore into a fresh optimizer over zeroed parameters
+    fresh = [torch.zeros_like(p) for p in _init_params()]
+    z2 = ZeroFlashOptimizer(fresh, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum")
+    z2.load_checkpoint(directory)
+    same = torch.equal(zo.flat_params.view(torch.int16), z2.flat_params.view(torch.int16)) and z2.t == zo.t
+    for a, b in zip(zo.states, z2.states):
+        same &= torch.equal(a.weights.corrections, b.weights.corrections)
+        same &= torch.equal(a.momentum.codes, b.momentum.codes)
+        same &= torch.equal(a.momentum.scales.view(torch.int16), b.momentum.scales.view(torch.int16))
+        if opt == "adamw":
+            same &= torch.equal(a.variance.codes, b.variance.codes)
+            same &= torch.equal(a.variance.scales.view(torch.int16), b.variance.scales.view(torch.int16))
+        same &= a.t == b.t
+    q.put((rank, bool(same)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("opt", ["adamw", "sgd", "lion"])
+def test_zero1_sharded_checkpoint(opt, oracle_mod, tmp_path):
+    """SURVEY.md §8e sharded checkpoints: the shards' state is gathered into
+    one FLOP v1 file per tensor, byte-identical to the file of the unsharded
+    oracle state, and reloads (re-sharded) bit for bit."""
+    from paper_2602_23349_b200 import optim as FO
+    from paper_2602_23349_b200.checkpoint import save_checkpoint
+    from paper_2602_23349_b200.host import HostFlashState
+
+    d = str(tmp_path / "ckpt")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_ckpt, args=(r, 2, port, opt, q, d)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: True, 1: True}
+    hp = {"adamw": [dict(lr=1e-3, beta2=0.95, weight_decay=0.1), dict(lr=1e-3)],
+          "sgd": [dict(lr=0.1, weight_decay=1e-4), dict(lr=0.1)],
+          "lion": [dict(lr=1e-4, weight_decay=0.1), dict(lr=1e-4)]}[opt]
+    hp = [{k: v for k, v in FO.HP_TYPES[opt](**h).__dict__.items()} for h in hp]
+    group_of = [0, 1, 0, 1, 1]
+    for i, p in enumerate(_init_params()):
+        lp = _np(p).copy()
+        n = lp.size
+        ng = -(-n // 32)
+        v = (np.zeros(n, np.uint8), np.zeros(ng, np.float16)) if opt == "adamw" else (None, None)
+        st = oracle_mod.OracleState(lp, np.zeros(n, np.int8), np.zeros(n, np.int8), np.zeros(ng, np.float16),
+                                    v[0], v[1], 0)
+        for s in range(STEPS):
+            assert oracle_mod.step_inplace(opt, st, _grads(s)[i].float().numpy(), **hp[group_of[i]]) == 0
+        ref = tmp_path / f"ref{i}.flop"
+        save_checkpoint(HostFlashState(st.lp, st.rho, st.m_codes, st.m_scales, st.v_codes, st.v_scales, st.t, 32),
+                        ref, opt)
+        with open(ref, "rb") as f1, open(os.path.join(d, f"{i:05d}.flop"), "rb") as f2:
+            assert f1.read() == f2.read(), i

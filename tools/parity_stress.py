@@ -45,8 +45,9 @@ def random_case(rng):
         hp = dict(lr=lr, beta1=pick_beta(rng), beta2=pick_beta(rng), weight_decay=wd)
     t = int(rng.choice([0, 1, int(rng.integers(2, 400)), int(rng.integers(400, 30000))]))
     lo, hi = sorted(rng.uniform(-149, 8, 2))
+    inject = str(rng.choice(["none"] * 9 + ["nan", "inf", "huge", "rho"])) if rng.random() < 0.3 else "none"
     return dict(opt=opt, n=n, hp=hp, t=t, glo=float(lo), ghi=float(hi), zero_state=bool(rng.random() < 0.2),
-                grad_f32=bool(rng.random() < 0.2), seed=int(rng.integers(0, 2 ** 31)))
+                grad_f32=bool(rng.random() < 0.2), inject=inject, seed=int(rng.integers(0, 2 ** 31)))
 
 
 def run_case(c, dev):
@@ -64,6 +65,15 @@ def run_case(c, dev):
     g[rng.random(n) < 0.01] = 0.0
     if not c["grad_f32"]:
         g = H.bf16_round(g)
+    k = rng.integers(0, n, max(1, n // 100000))
+    if c.get("inject") == "nan":
+        g[k] = np.float32("nan")
+    elif c.get("inject") == "inf":
+        g[k] = np.float32("-inf")
+    elif c.get("inject") == "huge":
+        g[k] = np.float32(3e38)
+    elif c.get("inject") == "rho":
+        st["weights.rho"][k] = -128
     ost = oracle_state(st, c["t"])
     oerr = O.step_inplace(opt, ost, g, nthreads=8, **c["hp"])
     fs = to_device(st, c["t"], dev)
