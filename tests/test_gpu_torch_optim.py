@@ -202,5 +202,27 @@ def test_zero1_single_rank_nccl_matches_oracle(cuda_dev, oracle_mod):
         torch.cuda.synchronize()
         for p, st in zip(params, ost):
             assert np.array_equal(p.view(torch.int16).cpu().numpy().view(np.uint16), st.lp)
+        # sharded checkpoint over NCCL: files byte-identical to the oracle state's, reload bit for bit
+        import tempfile
+
+        from paper_2602_23349_b200.checkpoint import save_checkpoint
+        from paper_2602_23349_b200.host import HostFlashState
+
+        with tempfile.TemporaryDirectory() as d:
+            zo.save_checkpoint(d)
+            for i, st in enumerate(ost):
+                ref = os.path.join(d, f"ref{i}.flop")
+                save_checkpoint(HostFlashState(st.lp, st.rho, st.m_codes, st.m_scales, st.v_codes, st.v_scales,
+                                               st.t, 32), ref, "adamw")
+                with open(ref, "rb") as f1, open(os.path.join(d, f"{i:05d}.flop"), "rb") as f2:
+                    assert f1.read() == f2.read(), i
+            fresh = [torch.zeros_like(p) for p in params]
+            z2 = ZeroFlashOptimizer(fresh, "adamw", [hp], reduce_op="sum")
+            z2.load_checkpoint(d)
+            assert torch.equal(z2.flat_params.view(torch.int16), zo.flat_params.view(torch.int16))
+            for a, b in zip(zo.states, z2.states):
+                assert torch.equal(a.weights.corrections, b.weights.corrections)
+                assert torch.equal(a.momentum.codes, b.momentum.codes)
+                assert torch.equal(a.variance.codes, b.variance.codes)
     finally:
         dist.destroy_process_group()
