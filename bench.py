@@ -279,7 +279,7 @@ def pcie_bound_s(h2d_bytes: float, d2h_bytes: float, pk: dict) -> float:
     return t
 
 
-def host_e2e(fl, grads_flat, opt, hp, t0, steps, warmup):
+def host_e2e(fl, grads_flat, opt, hp, t0, steps, warmup, chunk_elems: int = 1 << 26):
     """e2e: the same step through the C-ABI host-buffer entry point
     (fo_step_host): state + gradient in pinned host memory, H2D copy, fused
     step and D2H copy of the updated state inside the timed region."""
@@ -315,11 +315,11 @@ def host_e2e(fl, grads_flat, opt, hp, t0, steps, warmup):
         d2h += n * (2 + 1 + 1 + (1 if adam else 0)) + ng * 2 * (2 if adam else 1)
     alloc_s = time.perf_counter() - t_alloc
     for _ in range(warmup):
-        step_host(opt, states, grads, hp, chunk_elems=1 << 26, check=False)
+        step_host(opt, states, grads, hp, chunk_elems=chunk_elems, check=False)
     torch.cuda.synchronize()
     t = time.perf_counter()
     for _ in range(steps):
-        step_host(opt, states, grads, hp, chunk_elems=1 << 26, check=False)
+        step_host(opt, states, grads, hp, chunk_elems=chunk_elems, check=False)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t) / steps
     pk = pcie_peaks()
