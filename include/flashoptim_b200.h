@@ -10,11 +10,11 @@
  * device form of the same contract:
  *
  *   reference                                  C ABI
- *   optim.adamw_step(state, grad, hp)  :406    fo_adamw_step / fo_step_mt(FO_OPT_ADAMW)
- *   optim.sgd_step(state, grad, hp)    :385    fo_sgd_step   / fo_step_mt(FO_OPT_SGD)
- *   optim.lion_step(state, grad, hp)   :436    fo_lion_step  / fo_step_mt(FO_OPT_LION)
- *   optim.STEP_FUNCTIONS               :459    fo_step_mt's `optimizer` argument
- *   optim.init_flash_state             :341    fo_split + zeroed codes/scales
+ *   optim.adamw_step(state, grad, hp)  :208    fo_adamw_step / fo_step_mt(FO_OPT_ADAMW)
+ *   optim.sgd_step(state, grad, hp)    :187    fo_sgd_step   / fo_step_mt(FO_OPT_SGD)
+ *   optim.lion_step(state, grad, hp)   :238    fo_lion_step  / fo_step_mt(FO_OPT_LION)
+ *   optim.STEP_FUNCTIONS               :261    fo_step_mt's `optimizer` argument
+ *   optim.init_flash_state             :143    fo_split + zeroed codes/scales
  *   formats.split                      :232    fo_split
  *   formats.reconstruct                :248    fo_reconstruct
  *   quantize.quantize_momentum         :109    fo_quantize_momentum
@@ -48,7 +48,7 @@ extern "C" {
 #define FO_ETOOMANY (-3)     /* hyper-parameter table larger than FO_MAX_HPARAMS */
 
 /* Device error bits, one per reference ValueError class and buffer. */
-#define FO_ERR_GRAD_NONFINITE 0x01u  /* optim.py:381 "gradient-nonfinite" */
+#define FO_ERR_GRAD_NONFINITE 0x01u  /* optim.py:183 "gradient-nonfinite" */
 #define FO_ERR_RHO_INVALID 0x02u     /* formats.py:271 "invalid-correction-code" */
 #define FO_ERR_SPLIT_NONFINITE 0x04u /* formats.py:243 "split-nonfinite" */
 #define FO_ERR_M_NONFINITE 0x08u     /* quantize.py:69 "quantize-nonfinite" (momentum) */
@@ -63,11 +63,11 @@ extern "C" {
 #define FO_OPT_LION 2
 
 /* Gradient element types.  The reference upcasts any grad to f32
- * (optim.py:377); bf16 is the training-time layout, f32 the exact one. */
+ * (optim.py:179); bf16 is the training-time layout, f32 the exact one. */
 #define FO_GRAD_BF16 0
 #define FO_GRAD_F32 1
 
-/* Variance storage schemes (optim.py:362-373). */
+/* Variance storage schemes (optim.py:164-175). */
 #define FO_VAR_COMPANDED 0
 #define FO_VAR_LINEAR 1
 
@@ -76,7 +76,7 @@ extern "C" {
 /* Per-step float32 scalars, formed on the host exactly as the reference
  * forms them: Python floats rounded once to f32 (NEP 50), 1-beta and the
  * bias corrections 1-beta**t evaluated in float64 then rounded once
- * (optim.py:410-411, 418-419, 445-446).  Fill with fo_make_hparams(). */
+ * (optim.py:212-213, 220-221, 247-248).  Fill with fo_make_hparams(). */
 typedef struct fo_hparams {
   float lr, wd, eps;
   float b1, omb1; /* beta1 and f32(1-beta1)          (AdamW, Lion) */
@@ -108,10 +108,10 @@ uint32_t fo_abi_version(void);
 const char *fo_status_string(int status);
 /* Message of the reference ValueError that `mask` corresponds to for
  * `optimizer` (first in the reference's program order), or "" if mask==0.
- * Precedence: optim.py:406-433 (AdamW), :385-403 (SGD), :436-456 (Lion). */
+ * Precedence: optim.py:208-235 (AdamW), :187-205 (SGD), :238-258 (Lion). */
 const char *fo_error_message(uint32_t mask, int optimizer);
 
-/* Host helper: the reference's per-step f32 scalars (optim.py:408-424). */
+/* Host helper: the reference's per-step f32 scalars (optim.py:210-226). */
 void fo_make_hparams(int optimizer, double lr, double beta1, double beta2, double eps, double weight_decay,
                      double momentum, int64_t t, fo_hparams *out);
 
@@ -126,18 +126,36 @@ int fo_step_mt(int optimizer, const fo_tensor *tensors, int32_t n_tensors, const
                uint32_t *d_err, void *stream);
 
 /* Host-resident state (the reference's calling convention: NumPy arrays in
- * host memory, optim.py:385-459).  Every pointer in `tensors` is a HOST
+ * host memory, optim.py:187-261).  Every pointer in `tensors` is a HOST
  * pointer (pinned for full PCIe bandwidth; pageable works).  The list is cut
  * into group-aligned pieces that stream through `chunk_elems`-element device
  * slots (0 = 64M): H2D copy, fused step, D2H copy on three rotating slots
- * and streams.  Synchronous; the error mask is written to *h_err. */
+ * and streams.  Any group_size >= 1 (quantize.py:33-44); every piece keeps
+ * its own 16-byte aligned run of scales in the slot.  Synchronous; the error
+ * mask is written to *h_err.  Reentrant: each call leases its own slots and
+ * streams from a pool of per-device contexts, so concurrent calls from
+ * several host threads neither share buffers nor serialise. */
 int fo_step_host(int optimizer, const fo_tensor *tensors, int32_t n_tensors, const fo_hparams *hparams,
                  int32_t n_hparams, int grad_dtype, int rho_bits, int32_t group_size, int variance_scheme,
                  int64_t chunk_elems, uint32_t *h_err);
-/* Free the device slots fo_step_host keeps between calls. */
+/* Free the idle contexts (device slots and streams) fo_step_host keeps
+ * between calls. */
 void fo_host_release(void);
 
-/* Single-tensor steps, in place (optim.py:406, :385, :436). */
+/* Fast-path accounting of the fused launches on `stream` (current device).
+ * The fused kernel computes every 512-element slice with exact shortcuts
+ * whose preconditions it checks per slice; a slice whose check trips stores
+ * nothing and is re-run by the fix-up launch that follows on the same stream
+ * (DESIGN.md §3.2).  *flagged = slices re-run by fix-up launches, *slices =
+ * slices the fused launches covered, both since the last reset.  Synchronises
+ * `stream`.  No reference counterpart (test and bench support). */
+int fo_fixup_stats(void *stream, uint64_t *flagged, uint64_t *slices, int reset);
+/* Pre-size the fix-up bitmap of `stream` for launches of up to `max_elems`
+ * elements, so that a CUDA-graph capture of fo_step_mt on that stream
+ * allocates nothing.  Optional. */
+int fo_reserve(void *stream, int64_t max_elems);
+
+/* Single-tensor steps, in place (optim.py:208, :187, :238). */
 int fo_adamw_step(uint16_t *lp, int8_t *rho, int8_t *m_codes, uint16_t *m_scales, uint8_t *v_codes,
                   uint16_t *v_scales, const void *grad, int grad_dtype, int64_t n, const fo_hparams *hp,
                   uint32_t *d_err, void *stream);

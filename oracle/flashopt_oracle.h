@@ -12,7 +12,7 @@ extern "C" {
 
 /* Error bits: one per reference ValueError class and buffer.  Same values as
  * include/flashoptim_b200.h so tests can compare masks directly. */
-#define FO_ERR_GRAD_NONFINITE 0x01u  /* optim.py:381 "gradient-nonfinite" */
+#define FO_ERR_GRAD_NONFINITE 0x01u  /* optim.py:183 "gradient-nonfinite" */
 #define FO_ERR_RHO_INVALID 0x02u     /* formats.py:271 "invalid-correction-code" */
 #define FO_ERR_SPLIT_NONFINITE 0x04u /* formats.py:243 "split-nonfinite" */
 #define FO_ERR_M_NONFINITE 0x08u     /* quantize.py:69 "quantize-nonfinite" (momentum) */

@@ -3,7 +3,7 @@
 TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
 bench.py's cpu_baseline / --impl reference legs, never by the product
 package.  Mirrors the reference's functional API
-(/root/reference/pkg/src/flashopt/optim.py:385-459, formats.py:232-276,
+(/root/reference/pkg/src/flashopt/optim.py:187-261, formats.py:232-276,
 quantize.py:109-158) on plain NumPy arrays: inputs are copied, the copy is
 stepped in place by the C restatement, and errors are raised as ValueError
 with the reference's message prefixes.
@@ -32,7 +32,7 @@ ERR_V_OVERFLOW = 0x80
 
 OPT_TAGS = {"sgd": 0, "adamw": 1, "lion": 2}
 
-# Reference messages (optim.py:381, formats.py:243,271, quantize.py:69,85,144).
+# Reference messages (optim.py:183, formats.py:243,271, quantize.py:69,85,144).
 MESSAGES = {
     ERR_GRAD_NONFINITE: "gradient-nonfinite: gradient contains NaN/Inf",
     ERR_RHO_INVALID: "invalid-correction-code: asymmetric minimum is forbidden",
@@ -206,7 +206,7 @@ class OracleState:
 
 
 def init_state(theta0, optimizer: str, G: int = 32) -> OracleState:
-    """optim.py:341-359 init_flash_state."""
+    """optim.py:143-161 init_flash_state."""
     lp, rho = split(theta0)
     n = lp.size
     ng = _ngroups(n, G)

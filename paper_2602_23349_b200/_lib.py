@@ -77,6 +77,9 @@ SIGNATURES = {
     "fo_step_host": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(fo_tensor), _I32, ctypes.POINTER(fo_hparams), _I32,
                                     ctypes.c_int, ctypes.c_int, _I32, ctypes.c_int, _I64, ctypes.POINTER(_U32)]),
     "fo_host_release": (None, []),
+    "fo_fixup_stats": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
+                                      ctypes.c_int]),
+    "fo_reserve": (ctypes.c_int, [_P, _I64]),
 }
 
 _lib = None
@@ -121,6 +124,18 @@ def make_hparams(optimizer: str, lr: float, beta1: float = 0.9, beta2: float = 0
     lib().fo_make_hparams(OPT_TAGS[optimizer], lr, beta1, beta2, eps, weight_decay, momentum, int(t),
                           ctypes.byref(hp))
     return hp
+
+
+def fixup_stats(stream: int | None = None, reset: bool = False) -> tuple[int, int]:
+    """(slices re-run by fix-up launches, slices covered by fused launches)
+    on `stream` (a cudaStream_t handle; default: torch's current stream)."""
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream().cuda_stream
+    f, n = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    check(lib().fo_fixup_stats(stream, ctypes.byref(f), ctypes.byref(n), int(reset)), "fo_fixup_stats")
+    return int(f.value), int(n.value)
 
 
 def error_message(mask: int, optimizer: str) -> str:

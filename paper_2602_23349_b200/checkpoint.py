@@ -330,6 +330,14 @@ def load_optimizer(optimizer, directory) -> None:
             if list(p.shape) != ent["shape"]:
                 raise CheckpointError(f"shape mismatch for {ent['name']}")
             fs = load_checkpoint(os.path.join(directory, ent["file"]), device=p.device)
+            rec = {"weights.rho": fs.weights.corrections, "momentum.scales": fs.momentum.scales}
+            if fs.variance is not None:
+                rec["variance.scales"] = fs.variance.scales
+            if hasattr(optimizer, "_check_layout"):
+                try:
+                    optimizer._check_layout(p, rec)
+                except ValueError as e:
+                    raise CheckpointError(f"{ent['name']}: {e}") from None
             if p.dtype != torch.bfloat16:
                 p.data = torch.empty(p.shape, dtype=torch.bfloat16, device=p.device)
             p.data.view(-1).copy_(fs.weights.lp_values)

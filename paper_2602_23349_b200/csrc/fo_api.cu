@@ -12,7 +12,7 @@ namespace {
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 const char* kMsg[8] = {
-    "gradient-nonfinite: gradient contains NaN/Inf",                 // optim.py:381
+    "gradient-nonfinite: gradient contains NaN/Inf",                 // optim.py:183
     "invalid-correction-code: asymmetric minimum is forbidden",      // formats.py:271
     "split-nonfinite: cannot split NaN/Inf master weights",          // formats.py:243
     "quantize-nonfinite: state buffer contains NaN/Inf",             // quantize.py:69
@@ -71,8 +71,8 @@ void fo_make_hparams(int optimizer, double lr, double beta1, double beta2, doubl
   out->b2 = (float)beta2;
   out->omb2 = (float)(1.0 - beta2);
   out->mu = (float)momentum;
-  out->bc1 = (float)(1.0 - std::pow(beta1, (double)t));  // optim.py:410
-  out->bc2 = (float)(1.0 - std::pow(beta2, (double)t));  // optim.py:411
+  out->bc1 = (float)(1.0 - std::pow(beta1, (double)t));  // optim.py:212
+  out->bc2 = (float)(1.0 - std::pow(beta2, (double)t));  // optim.py:213
   volatile float one = 1.0f;                                // f32 division: RN(1/bc)
   out->rbc1 = one / out->bc1;
   out->rbc2 = one / out->bc2;
@@ -120,6 +120,15 @@ int fo_step_host(int optimizer, const fo_tensor* tensors, int32_t n_tensors, con
 }
 
 void fo_host_release(void) { fo::host_release(); }
+
+int fo_fixup_stats(void* stream, uint64_t* flagged, uint64_t* slices, int reset) {
+  return fo::fix_stats(as_stream(stream), flagged, slices, reset);
+}
+
+int fo_reserve(void* stream, int64_t max_elems) {
+  if (max_elems < 0) return FO_EINVAL;
+  return fo::fix_reserve(as_stream(stream), max_elems);
+}
 
 int fo_adamw_step(uint16_t* lp, int8_t* rho, int8_t* m_codes, uint16_t* m_scales, uint8_t* v_codes,
                   uint16_t* v_scales, const void* grad, int grad_dtype, int64_t n, const fo_hparams* hp,

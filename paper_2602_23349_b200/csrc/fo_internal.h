@@ -24,6 +24,21 @@ int quantize(bool variance, const float* x, int64_t n, int64_t G, void* codes, u
 int step_host(int opt, const fo_tensor* ts, int32_t nt, const fo_hparams* hps, int32_t nhp, int grad_dtype,
               int rho_bits, int32_t G, int var_scheme, int64_t chunk_elems, uint32_t* h_err);
 void host_release();
+
+// Fix-up bitmap of one (device, stream): one bit per 512-element slice of a
+// fused launch whose guards tripped, plus a device counter of the slices the
+// fix-up launches re-ran.  Shared by the three optimizer translation units
+// (fo_step.cu).  `bits` is NULL when allocation failed.
+struct FixBuf {
+  uint32_t* bits;
+  unsigned long long* count;
+};
+FixBuf fix_buffer(cudaStream_t s, size_t words);
+void fix_account(cudaStream_t s, uint64_t slices);  // host-side count of fast-tile slices launched
+int fix_stats(cudaStream_t s, uint64_t* flagged, uint64_t* slices, int reset);
+int fix_reserve(cudaStream_t s, int64_t elems);
+// Persistent-grid size of `kernel` on the current device (cached per kernel and device).
+int grid_cap_for(const void* kernel, int threads, int smem);
 int selftest(int mode, uint64_t begin, uint64_t count, unsigned long long* d_out, cudaStream_t s);
 int sweep(int block0, int nblocks, uint32_t scheme_mask, void* out, cudaStream_t s);
 int dequantize(bool variance, const void* codes, const uint16_t* scales, int64_t n, int64_t G, float* out,

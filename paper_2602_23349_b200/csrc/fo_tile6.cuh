@@ -2,7 +2,7 @@
 // kernel), included by fo_step_impl.cuh.
 //
 // Bit-identical to process_tile_exact (and therefore to the reference,
-// optim.py:385-459) whenever no guard trips; a tripped guard anywhere in the
+// optim.py:187-261) whenever no guard trips; a tripped guard anywhere in the
 // warp sends the whole tile to process_tile_exact before anything is
 // stored.  Differences from compute_tile (the older kernels' tile):
 //
@@ -338,7 +338,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const int j = 2 * k;
     if ((k & 3) == 0) {
       in.half(k >> 2, hl, hg, hr, hm, hv);
-      if (SAFE) {  // only non-finite gradients matter here (optim.py:380-381)
+      if (SAFE) {  // only non-finite gradients matter here (optim.py:182-183)
         if (sizeof(GradT) == 2) {
 #pragma unroll
           for (int q = 0; q < NGH; ++q) gnf |= __vcmpeq2(hg[q] & 0x7F807F80u, 0x7F807F80u);
@@ -381,7 +381,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     } else {
       g2 = make_float2(__uint_as_float(hg[j & 7]), __uint_as_float(hg[(j & 7) + 1]));
     }
-    // update (optim.py:393-396, :418-424, :445-447)
+    // update (optim.py:195-198, :220-226, :247-249)
     float2 m2, tn2;
     if (OPT == FO_OPT_ADAMW) {
       const float2 z2 = make_float2(L.v(vwd, j & 3), L.v(vwd, (j & 3) + 1));

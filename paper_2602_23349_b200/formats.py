@@ -23,7 +23,7 @@ from ._errors import DeviceErrors, ptr, stream_handle
 __all__ = ["BF16", "INT8_CORRECTION", "INT16_CORRECTION", "CorrectionWidth", "SplitTensor", "split",
            "reconstruct", "upcast"]
 
-BF16 = "bf16"  # the only low-precision weight format a FlashState uses (optim.py:353, checkpoint.py:251)
+BF16 = "bf16"  # the only low-precision weight format a FlashState uses (optim.py:155, checkpoint.py:251)
 
 
 @dataclass(frozen=True)

@@ -2,7 +2,7 @@
 
 This is the reference's own calling convention -- the state and the
 gradient are NumPy arrays in host memory and `adamw_step(state, grad, hp)`
-updates them (optim.py:385-459) -- executed by the CUDA library: the arrays
+updates them (optim.py:187-261) -- executed by the CUDA library: the arrays
 are streamed through device slots (H2D copy, fused step, D2H copy) with the
 copies overlapping the kernels.  Use `pinned_state` for full PCIe bandwidth.
 """

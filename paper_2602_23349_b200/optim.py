@@ -189,7 +189,7 @@ def step_many(optimizer: str, states: Sequence[FlashState], grads: Sequence[torc
     """Step every (state, grad) pair in place, fused into as few kernel
     launches as the layouts allow (one per FO_MT_MAX_TENSORS tensors for the
     fast layout).  `hps` is one hyper-parameter object or one per state.
-    Each state's step counter t is incremented (optim.py:409).  Errors are
+    Each state's step counter t is incremented (optim.py:211).  Errors are
     ORed into `errors` (not checked here)."""
     if optimizer not in OPTIMIZERS:
         raise ValueError(f"unknown optimizer: {optimizer}")

@@ -25,8 +25,12 @@ so the model trains on bf16 weights while the optimizer keeps 24-bit master
 weights.  bf16 parameters start with zero corrections.
 
 All parameters of a param group go to the GPU in one fused launch per step
-(fo_step_mt); errors are checked after the step (one device-to-host read)
-unless `check_errors=False`.
+(fo_step_mt).  Errors (the reference's ValueErrors) are flagged by the
+kernels in a device word; `check_errors` chooses when the host reads it:
+"deferred" (default: copied asynchronously after each step and raised by
+the next step() once it has arrived, never blocking), True / "sync" (read
+after every step, which waits for the step) or False (only when
+raise_errors() is called).  See _errors.ErrorPolicy.
 """
 
 from __future__ import annotations
@@ -37,7 +41,7 @@ from typing import Iterable
 import torch
 
 from . import _lib
-from ._errors import DeviceErrors, raise_for_mask, stream_handle
+from ._errors import DeviceErrors, ErrorPolicy, raise_for_mask, stream_handle
 from .formats import INT8_CORRECTION, SplitTensor, split
 from .optim import AdamHyperParams, FlashState, LionHyperParams, SgdHyperParams
 from .quantize import GroupSpec, QuantizedState
@@ -52,7 +56,9 @@ class FlashOptimizer(torch.optim.Optimizer):
 
     OPT = ""
 
-    def __init__(self, params, defaults: dict, *, check_errors: bool = True, group_size: int = 32):
+    def __init__(self, params, defaults: dict, *, check_errors: bool | str = "deferred", group_size: int = 32):
+        if check_errors not in (True, False, None, "sync", "deferred", "off"):
+            raise ValueError(f"check_errors must be True, False, 'sync', 'deferred' or 'off', got {check_errors!r}")
         self.check_errors = check_errors
         self.spec = GroupSpec(group_size)
         super().__init__(params, defaults)
@@ -60,7 +66,7 @@ class FlashOptimizer(torch.optim.Optimizer):
             self.hp(group)  # validate with the reference's rules
             for p in group["params"]:
                 self._init_state(p)
-        self._errors: DeviceErrors | None = None
+        self._errors: ErrorPolicy | None = None
         self._plans: dict = {}
 
     # -- state -----------------------------------------------------------------
@@ -102,8 +108,20 @@ class FlashOptimizer(torch.optim.Optimizer):
         raise NotImplementedError
 
     # -- step ------------------------------------------------------------------
-    def _launch(self, params: list, grads: list, group: dict, stream=None, errors: DeviceErrors | None = None):
-        """One fused launch for `params` (all from `group`)."""
+    def _rho_bits(self, p: torch.Tensor) -> int:
+        return self.state[p]["weights.rho"].element_size() * 8
+
+    def _launch(self, params: list, grads: list, group: dict, stream=None, errors=None):
+        """One fused launch for `params` (all from `group`), split by
+        correction width (int8, or int16 loaded from an INT16_CORRECTION
+        checkpoint, formats.py:94-95)."""
+        widths = {self._rho_bits(p) for p in params}
+        if len(widths) > 1:
+            for w in sorted(widths):
+                sel = [(p, g) for p, g in zip(params, grads) if self._rho_bits(p) == w]
+                self._launch([p for p, _ in sel], [g for _, g in sel], group, stream, errors)
+            return
+        rho_bits = widths.pop() if widths else 8
         hp = self.hp(group)
         tensors, scalars, index, keep = [], [], {}, []
         gdt = None
@@ -133,7 +151,7 @@ class FlashOptimizer(torch.optim.Optimizer):
         errs = errors or self._errors
         _lib.check(_lib.lib().fo_step_mt(
             _lib.OPT_TAGS[self.OPT], arr, len(tensors), hp_arr, len(scalars),
-            _lib.FO_GRAD_BF16 if gdt == torch.bfloat16 else _lib.FO_GRAD_F32, 8, self.spec.group_size,
+            _lib.FO_GRAD_BF16 if gdt == torch.bfloat16 else _lib.FO_GRAD_F32, rho_bits, self.spec.group_size,
             _lib.FO_VAR_COMPANDED, errs.ptr if errs is not None else None, sh), "fo_step_mt")
         if stream is not None:
             for g in keep:
@@ -150,7 +168,8 @@ class FlashOptimizer(torch.optim.Optimizer):
         grads = []
         for p in ps:
             g = p.grad
-            if g.dtype != torch.bfloat16 or not g.is_contiguous() or int(self.state[p]["step"]) != t0:
+            if g.dtype != torch.bfloat16 or not g.is_contiguous() or int(self.state[p]["step"]) != t0 \
+                    or self.state[p]["weights.rho"].dtype != torch.int8:
                 return False
             grads.append(g)
         key = (tuple(id(p) for p in ps), tuple(p.data_ptr() for p in ps))
@@ -194,23 +213,38 @@ class FlashOptimizer(torch.optim.Optimizer):
             if not ps:
                 continue
             dev = ps[0].device
-            if self._errors is None or self._errors.word.device != dev:
-                self._errors = DeviceErrors(dev)
+            if self._errors is None or self._errors.errors.word.device != dev:
+                self._errors = ErrorPolicy(self.check_errors, dev)
             if not self._launch_cached(gi, group, ps):
                 self._launch(ps, [p.grad.reshape(-1) for p in ps], group)
-        if self.check_errors and dev is not None:
-            self.raise_errors()
+        if dev is not None:
+            self._errors.after_step(self.OPT)
         return loss
 
     def raise_errors(self) -> None:
         """Raise the reference's ValueError for any error the kernels flagged
-        since the last check (one device-to-host read)."""
+        since the last check (waits for the queued steps)."""
         if self._errors is None:
             return
-        m = self._errors.mask()
-        if m:
-            self._errors.reset()
-            raise_for_mask(m, self.OPT)
+        self._errors.raise_now(self.OPT)
+
+    def _check_layout(self, p: torch.Tensor, st: dict) -> None:
+        """A loaded state must match the optimizer's layout: its group size
+        (scales hold ceil(n/G) entries) and a correction width the kernels take
+        (int8, or int16 from INT16_CORRECTION, formats.py:94-95)."""
+        n = p.numel()
+        rho = st.get("weights.rho")
+        if rho is not None:
+            if rho.dtype not in (torch.int8, torch.int16):
+                raise ValueError(f"weights.rho must be int8 or int16, got {rho.dtype}")
+            if rho.numel() != n:
+                raise ValueError(f"weights.rho has {rho.numel()} elements, parameter has {n}")
+        ng = self.spec.num_groups(n)
+        for k in ("momentum.scales", "variance.scales"):
+            v = st.get(k)
+            if v is not None and v.numel() != ng:
+                raise ValueError(f"{k} has {v.numel()} entries; group size {self.spec.group_size} needs {ng} "
+                                 "(checkpoint written with another group size)")
 
     # -- torch.optim plumbing ----------------------------------------------------
     # torch.optim.Optimizer.load_state_dict casts floating-point state to the
@@ -243,6 +277,7 @@ class FlashOptimizer(torch.optim.Optimizer):
                 id_map[pid] = p
         for pid, st in saved.items():
             p = id_map[pid]
+            self._check_layout(p, st)
             if p.dtype == torch.float32:  # a fresh model: the checkpoint holds bf16 weights.lp
                 p.data = p.data.to(torch.bfloat16)
             new = {}

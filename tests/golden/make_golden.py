@@ -6,7 +6,7 @@ The fixtures travel with the repo; the GPU box and the CPU tests compare
 against them without the reference.  Every case records the reference
 inputs (FLOP v1 record names, gradient, hyper-parameters, step counter) and
 the reference outputs (`out.<record>`), produced by
-flashopt.optim.STEP_FUNCTIONS (optim.py:459) and the codecs of
+flashopt.optim.STEP_FUNCTIONS (optim.py:261) and the codecs of
 flashopt.formats / flashopt.quantize.
 """
 

@@ -5,7 +5,7 @@ A "random valid state" is what SURVEY.md §7.1 asks for: bf16 weight codes
 with in-range corrections rho in [-127, 127], momentum codes in [-127, 127],
 variance codes in [0, 255] and finite non-negative fp16 group scales, plus
 bf16-representable gradients (the reference upcasts grads to f32,
-optim.py:376-382).
+optim.py:178-184).
 """
 
 from __future__ import annotations

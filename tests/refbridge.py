@@ -1,8 +1,12 @@
-"""Bridge to the live NumPy reference (/root/reference/pkg/src/flashopt).
+"""Bridge to the live NumPy reference (flashopt).
 
-Only available in the build container (the reference does not travel to
-the GPU box); tests that use it skip when it is absent.  Used to pin the C
-oracle and to generate tests/golden/ fixtures.
+Looked up in baseline/_ref first -- the unmodified reference installed with
+pip; it is git-ignored but travels to the GPU box with the
+repo snapshot -- then in /root/reference/pkg/src (build container only).
+Tests that use it skip when neither is present.  Used to pin the C oracle,
+to generate tests/golden/ fixtures and to check the reference-side binding
+(paper_2602_23349_b200/flashopt_binding.py) against the reference's own
+NumPy output on the GPU box.
 """
 
 from __future__ import annotations
@@ -12,7 +16,9 @@ import sys
 
 import numpy as np
 
-REF_SRC = "/root/reference/pkg/src"
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+_CANDIDATES = (os.path.join(_ROOT, "baseline", "_ref"), "/root/reference/pkg/src")
+REF_SRC = next((p for p in _CANDIDATES if os.path.isdir(os.path.join(p, "flashopt"))), _CANDIDATES[-1])
 
 
 def available() -> bool:

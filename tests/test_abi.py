@@ -1,7 +1,7 @@
 """CPU: the C-ABI library loads, exports every entry point include/*.h
 declares, and its host-side helpers (no GPU needed) behave like the
-reference: f32 step scalars (optim.py:408-424), error-message precedence
-(optim.py:385-456) and synchronous argument validation."""
+reference: f32 step scalars (optim.py:210-226), error-message precedence
+(optim.py:187-258) and synchronous argument validation."""
 
 from __future__ import annotations
 
@@ -50,7 +50,7 @@ def test_abi_version_and_status_strings():
 @pytest.mark.parametrize("beta1,beta2,t", [(0.9, 0.999, 1), (0.9, 0.95, 10), (0.85, 0.9999, 4321), (0.0, 0.5, 3)])
 def test_make_hparams_matches_python_float_semantics(beta1, beta2, t):
     """f32(1 - beta**t) computed in float64 then rounded once, like
-    np.float32(1.0 - hp.beta1**t) in optim.py:410-411; f32(1-beta) like the
+    np.float32(1.0 - hp.beta1**t) in optim.py:212-213; f32(1-beta) like the
     NEP-50 promotion of (1.0 - hp.beta1) * f32 array."""
     from paper_2602_23349_b200 import _lib
 
@@ -73,7 +73,7 @@ def test_error_message_precedence():
     assert msg(0, "adamw") == ""
     assert msg(E.ERR_GRAD_NONFINITE | E.ERR_M_OVERFLOW, "adamw").startswith("gradient-nonfinite")
     assert msg(E.ERR_RHO_INVALID | E.ERR_SPLIT_NONFINITE, "lion").startswith("invalid-correction-code")
-    # SGD quantises momentum before reconstructing (optim.py:393-395)
+    # SGD quantises momentum before reconstructing (optim.py:195-197)
     assert msg(E.ERR_RHO_INVALID | E.ERR_M_OVERFLOW, "sgd").startswith("scale-overflow")
     assert msg(E.ERR_RHO_INVALID | E.ERR_M_OVERFLOW, "adamw").startswith("invalid-correction-code")
     assert msg(E.ERR_M_OVERFLOW | E.ERR_V_NONFINITE, "adamw").startswith("scale-overflow")

@@ -68,6 +68,38 @@ def test_fused_step_1m_and_odd(opt, cuda_dev, oracle_mod):
 
 
 @pytest.mark.parametrize("opt", OPTS)
+def test_fast_path_share(opt, cuda_dev, oracle_mod):
+    """The fused tile, not the fix-up re-run, computes the parity cases: on a
+    state with training-like weights (N(0, 0.02^2), no +-0 codes) at least 99%
+    of the 512-element slices are stored by the fast tile (fo_fixup_stats),
+    and the result is still bitwise equal to the oracle.  The standard random
+    state (0.5% exact zeros, magnitudes down to 1e-40) sends most slices to
+    the fix-up launch; both paths are covered."""
+    from paper_2602_23349_b200 import _lib
+
+    rng = np.random.default_rng(4242 + OPTS.index(opt))
+    n = (1 << 21) + 12345
+    lp = H.bf16_codes((rng.standard_normal(n) * 0.02).astype(np.float32))
+    st = H.random_state(rng, n, opt, lp=lp)
+    g = H.random_grad(rng, n)
+    hp = dict(lr=1e-5, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1) if opt == "adamw" else \
+        H.random_hparams(rng, opt)
+    _lib.fixup_stats(reset=True)
+    mm = _run_pair(opt, st, g, 1000, hp, cuda_dev, oracle_mod)
+    flagged, slices = _lib.fixup_stats(reset=True)
+    assert all(v == 0 for v in mm.values()), mm
+    assert slices >= n // 512, (flagged, slices)
+    assert flagged <= 0.01 * slices, (flagged, slices)
+
+    st2 = H.random_state(rng, 1 << 20, opt)
+    g2 = H.random_grad(rng, 1 << 20)
+    mm = _run_pair(opt, st2, g2, 10, hp, cuda_dev, oracle_mod)
+    flagged2, slices2 = _lib.fixup_stats(reset=True)
+    assert all(v == 0 for v in mm.values()), mm
+    assert 0 < flagged2 <= slices2
+
+
+@pytest.mark.parametrize("opt", OPTS)
 def test_f32_gradients(opt, cuda_dev, oracle_mod):
     """f32 grads that are not bf16-representable (the reference's own input type)."""
     rng = np.random.default_rng(5)

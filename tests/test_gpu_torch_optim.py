@@ -226,3 +226,81 @@ def test_zero1_single_rank_nccl_matches_oracle(cuda_dev, oracle_mod):
                 assert torch.equal(a.variance.codes, b.variance.codes)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["sync", "deferred", "off"])
+def test_error_policies(mode, cuda_dev):
+    """check_errors: "sync" raises inside the failing step; "deferred" (the
+    default) never blocks and raises from a later step() or raise_errors();
+    "off" only from raise_errors().  The message is the reference's."""
+    import paper_2602_23349_b200.torch_optim as TO
+
+    p = torch.nn.Parameter(torch.randn(4096, device="cuda", dtype=torch.bfloat16))
+    opt = TO.FlashAdamW([p], lr=1e-3, check_errors=mode)
+    p.grad = torch.full_like(p, float("nan"))
+    if mode == "sync":
+        with pytest.raises(ValueError, match="gradient-nonfinite"):
+            opt.step()
+        return
+    opt.step()  # queued; nothing blocks
+    p.grad = torch.zeros_like(p)
+    if mode == "deferred":
+        torch.cuda.synchronize()
+        with pytest.raises(ValueError, match="gradient-nonfinite"):
+            opt.step()
+    else:
+        opt.step()
+        with pytest.raises(ValueError, match="gradient-nonfinite"):
+            opt.raise_errors()
+    opt.raise_errors()  # cleared after being reported
+
+
+def test_default_step_does_not_sync(cuda_dev):
+    """The default policy issues no blocking device-to-host read: a step is
+    enqueued while the device is still busy with earlier work."""
+    import paper_2602_23349_b200.torch_optim as TO
+
+    p = torch.nn.Parameter(torch.randn(1 << 20, device="cuda", dtype=torch.bfloat16))
+    opt = TO.FlashAdamW([p], lr=1e-3)
+    p.grad = torch.randn_like(p) * 1e-3
+    opt.step()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)  # ~0.1 s of device work ahead of the step
+    done = torch.cuda.Event()
+    opt.step()
+    done.record()
+    assert not done.query()  # step() returned before the queued work finished
+    torch.cuda.synchronize()
+    opt.raise_errors()
+
+
+def test_int16_checkpoint_layout_in_torch_optimizer(cuda_dev, oracle_mod, tmp_path):
+    """A state loaded with int16 corrections (INT16_CORRECTION checkpoint) is
+    stepped with the int16 layout; a group-size mismatch is refused."""
+    import paper_2602_23349_b200.torch_optim as TO
+
+    rng = np.random.default_rng(3)
+    n = 5000
+    st = H.random_state(rng, n, "adamw", rho=rng.integers(-32767, 32768, n).astype(np.int16))
+    p = torch.nn.Parameter(torch.from_numpy(st["weights.lp"].view(np.int16)).cuda().view(torch.bfloat16))
+    opt = TO.FlashAdamW([p], lr=1e-3, betas=(0.9, 0.95), weight_decay=0.1, check_errors=True)
+    sd = opt.state_dict()
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
+    sd["state"][0].update({"weights.rho": T(st["weights.rho"]), "momentum.codes": T(st["momentum.codes"]),
+                           "momentum.scales": T(st["momentum.scales"]).view(torch.int16),
+                           "variance.codes": T(st["variance.codes"]),
+                           "variance.scales": T(st["variance.scales"]).view(torch.int16), "step": 7})
+    opt.load_state_dict(sd)
+    g = H.random_grad(rng, n)
+    p.grad = torch.from_numpy(g).cuda().to(torch.bfloat16)
+    opt.step()
+    from devstate import oracle_state
+
+    ost = oracle_state(st, 7)
+    assert oracle_mod.step_inplace("adamw", ost, g, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8,
+                                   weight_decay=0.1) == 0
+    mm = mismatches(_state_dict_np(opt, p), oracle_dict(ost))
+    assert all(v == 0 for v in mm.values()), mm
+    opt2 = TO.FlashAdamW([torch.nn.Parameter(p.detach().clone())], lr=1e-3, group_size=64)
+    with pytest.raises(ValueError, match="group size"):
+        opt2.load_state_dict(opt.state_dict())

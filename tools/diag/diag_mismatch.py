@@ -1,8 +1,9 @@
 """Debug helper: run one fused step vs the oracle and print the first mismatches."""
+import os
 import sys
 import numpy as np
 import torch
-sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
+_R = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))); sys.path.insert(0, _R); sys.path.insert(0, os.path.join(_R, "tests"))
 import helpers as H
 from devstate import from_device, oracle_dict, oracle_state, to_device, bits
 from oracle import oracle as O
