@@ -3,22 +3,30 @@
 Layout: every parameter is a view into one flat bf16 buffer,
 each tensor padded with zeros to a multiple of 32 so groups never straddle
 tensors (padding is a fixed point of all three steps: SURVEY Appendix B
-probe 13, tests/test_oracle_golden.py), and the total padded to a multiple of
-`ALIGN * world`.  Rank r owns the contiguous slice [r*L/W, (r+1)*L/W) of the
-flat buffer and allocates the correction / moment codes and scales only for
-that slice -- the paper's "rho remains local with the optimizer states"
-(PAPER.md:358-360).  One step is
+probe 13, tests/test_oracle_golden.py).  The flat buffer is cut into
+buckets (one bucket by default); each bucket is split into W equal pieces
+and rank r owns piece r of every bucket, allocating the correction / moment
+codes and scales only for what it owns -- the paper's "rho remains local
+with the optimizer states".  One step is
 
-    reduce-scatter(flat bf16 grads) -> fused step on the shard -> all-gather(flat bf16 params)
+    reduce-scatter(bf16 grads, per bucket) -> fused step on the owned pieces
+        -> all-gather(bf16 params, per bucket, in place)
 
-The step on a slice is bit-identical to stepping the full tensors on one GPU
+The step on a piece is bit-identical to stepping the full tensors on one GPU
 because every operation is elementwise or reduces within one group
-(SURVEY Appendix B probe 6).  Only the rank's shard of the grads is
-materialised after the reduce-scatter.
+(SURVEY Appendix B probe 6).  Only the owned pieces of the gradients are
+kept after the reduce-scatter.
+
+With `overlap_grad_reduce=True` a post-accumulate-grad hook counts the
+gradients that have arrived per bucket and launches that bucket's
+reduce-scatter asynchronously as soon as it is complete, so the exchange
+runs under the rest of the backward pass; step() only waits for it.
 
 `step_fn` is pluggable so the sharding and collective logic can be tested
 with the gloo backend on CPU (tests/test_zero_gloo.py); on GPUs the default
-is the fused CUDA step (paper_2602_23349_b200.optim.step_many).
+is the fused CUDA step through a cached launch table (flat.StepPlan).  With
+gloo and CUDA tensors the collectives are staged through host memory (a test
+mode: two processes can then share one GPU and still run the CUDA step).
 """
 
 from __future__ import annotations
@@ -29,7 +37,7 @@ from typing import Callable, Sequence
 import torch
 import torch.distributed as dist
 
-ALIGN = 512  # shard boundaries are tile- and group-aligned
+ALIGN = 512  # piece boundaries are tile- and group-aligned
 
 
 def shard_range(n: int, rank: int, world: int, align: int = 64) -> tuple[int, int]:
@@ -42,19 +50,20 @@ def shard_range(n: int, rank: int, world: int, align: int = 64) -> tuple[int, in
 
 @dataclass
 class Segment:
-    """A run of the rank's shard that belongs to one parameter."""
+    """A run of the rank's owned elements that belongs to one parameter."""
 
     param_index: int
-    shard_off: int    # offset inside the rank's shard
+    shard_off: int    # offset inside the rank's shard (concatenated pieces)
     tensor_off: int   # offset inside the parameter (multiple of 32)
     length: int       # real (unpadded) elements of the parameter in this run
     hp_index: int
+    flat_off: int = 0  # offset inside the flat buffer
 
 
 class FlatLayout:
-    """Offsets of every parameter in the padded flat buffer."""
+    """Offsets of every parameter in the padded flat buffer and its buckets."""
 
-    def __init__(self, numels: Sequence[int], world: int, group: int = 32):
+    def __init__(self, numels: Sequence[int], world: int, group: int = 32, bucket_elems: int | None = None):
         self.numels = [int(n) for n in numels]
         self.offsets = []
         off = 0
@@ -65,82 +74,231 @@ class FlatLayout:
         self.total = -(-off // unit) * unit if off else unit
         self.world = world
         self.shard = self.total // world
+        b = self.total if not bucket_elems else max(unit, -(-int(bucket_elems) // unit) * unit)
+        self.buckets = [(s, min(b, self.total - s)) for s in range(0, self.total, b)]  # (start, size)
+        self.piece_off = []  # shard offset of each bucket's piece
+        so = 0
+        for _, size in self.buckets:
+            self.piece_off.append(so)
+            so += size // world
+
+    def piece(self, k: int, rank: int) -> tuple[int, int]:
+        """Flat range [lo, hi) of bucket k owned by `rank`."""
+        s, size = self.buckets[k]
+        per = size // self.world
+        return s + rank * per, s + (rank + 1) * per
 
     def segments(self, rank: int, hp_index: Sequence[int]) -> list[Segment]:
-        lo, hi = rank * self.shard, (rank + 1) * self.shard
         segs = []
-        for i, (o, n) in enumerate(zip(self.offsets, self.numels)):
-            a, b = max(lo, o), min(hi, o + n)
-            if a < b:
-                segs.append(Segment(i, a - lo, a - o, b - a, int(hp_index[i])))
+        for k in range(len(self.buckets)):
+            lo, hi = self.piece(k, rank)
+            for i, (o, n) in enumerate(zip(self.offsets, self.numels)):
+                a, b = max(lo, o), min(hi, o + n)
+                if a < b:
+                    segs.append(Segment(i, self.piece_off[k] + a - lo, a - o, b - a, int(hp_index[i]), a))
         return segs
+
+    def buckets_of(self, i: int) -> list[int]:
+        o, n = self.offsets[i], self.numels[i]
+        return [k for k, (s, size) in enumerate(self.buckets) if s < o + n and o < s + size]
 
 
 class ZeroFlashOptimizer:
     """ZeRO-1 FlashSGD / FlashAdamW / FlashLion over a process group.
 
-    params      : bf16 tensors, identical on every rank (they are re-pointed
-                  into the flat buffer; gradients go to a flat grad buffer).
+    params      : bf16 (or fp32, CUDA) tensors, identical on every rank;
+                  they are re-pointed into the flat buffer and their .grad
+                  into a flat grad buffer.  fp32 parameters are split once
+                  into bf16 + int8 correction (init_flash_state,
+                  optim.py:143-161) like FlashAdamW does.
     hparams     : one hyper-parameter object per param group; `group_of[i]`
                   is parameter i's group.
+    check_errors: error policy of the fused step (see _errors.ErrorPolicy).
     """
 
     def __init__(self, params: Sequence[torch.Tensor], optimizer: str, hparams: Sequence, group_of=None,
-                 process_group=None, step_fn: Callable | None = None, reduce_op: str = "avg"):
+                 process_group=None, step_fn: Callable | None = None, reduce_op: str = "avg",
+                 bucket_elems: int | None = None, overlap_grad_reduce: bool = False,
+                 check_errors: bool | str = "deferred"):
         from .flat import FlatStates
 
         self.pg = process_group
         self.world = dist.get_world_size(self.pg)
         self.rank = dist.get_rank(self.pg)
+        self.backend = dist.get_backend(self.pg)
         self.optimizer = optimizer
         self.params = list(params)
         self.hparams = list(hparams)
         self.group_of = list(group_of) if group_of is not None else [0] * len(self.params)
         dev = self.params[0].device
-        self.layout = FlatLayout([p.numel() for p in self.params], self.world)
+        self.device = dev
+        if overlap_grad_reduce and bucket_elems is None:
+            bucket_elems = 1 << 26
+        self.layout = FlatLayout([p.numel() for p in self.params], self.world, bucket_elems=bucket_elems)
         L = self.layout
         self.flat_params = torch.zeros(L.total, dtype=torch.bfloat16, device=dev)
         self.flat_grads = torch.zeros(L.total, dtype=torch.bfloat16, device=dev)
-        for p, o in zip(self.params, L.offsets):
-            self.flat_params[o:o + p.numel()].copy_(p.detach().reshape(-1))
-            p.data = self.flat_params[o:o + p.numel()].view_as(p)
-            p.grad = self.flat_grads[o:o + p.numel()].view_as(p)
-        lo = self.rank * L.shard
-        self.shard_params = self.flat_params[lo:lo + L.shard]
+        split_rho = {}
+        with torch.no_grad():
+            for i, (p, o) in enumerate(zip(self.params, L.offsets)):
+                src = p.detach().reshape(-1)
+                if p.dtype == torch.float32:
+                    from .formats import split
+
+                    lp, rho = split(src)  # init_flash_state: fp32 -> bf16 + int8 rho (raises like the reference)
+                    self.flat_params[o:o + p.numel()].copy_(lp)
+                    split_rho[i] = rho
+                elif p.dtype == torch.bfloat16:
+                    self.flat_params[o:o + p.numel()].copy_(src)
+                else:
+                    raise TypeError(f"parameters must be bf16 or fp32, got {p.dtype}")
+                p.data = self.flat_params[o:o + p.numel()].view(p.shape)
+                p.grad = self.flat_grads[o:o + p.numel()].view(p.shape)
+        self._grad_views = [self.flat_grads[o:o + p.numel()].view(p.shape) for p, o in zip(self.params, L.offsets)]
         self.shard_grads = torch.zeros(L.shard, dtype=torch.bfloat16, device=dev)
         self.segments = L.segments(self.rank, self.group_of)
-        # optimizer state for the shard only, one FlashState per segment
+        # optimizer state for the owned pieces only, one FlashState per segment
         sizes = [s.length for s in self.segments]
-        views = [self.shard_params[s.shard_off:s.shard_off + s.length] for s in self.segments]
+        views = [self.flat_params[s.flat_off:s.flat_off + s.length] for s in self.segments]
         self.flat_state = FlatStates(sizes, optimizer, dev, lp_views=views) if sizes else None
         self.states = self.flat_state.states if sizes else []
+        for seg, st in zip(self.segments, self.states):
+            if seg.param_index in split_rho:
+                a = seg.tensor_off
+                st.weights.corrections.copy_(split_rho[seg.param_index][a:a + seg.length])
         self.step_fn = step_fn
         self.reduce_op = reduce_op
         self.t = 0
+        self._plan = None
+        self._errors = None
+        self.check_errors = check_errors
+        if dev.type == "cuda" and step_fn is None:
+            from ._errors import ErrorPolicy
+
+            self._errors = ErrorPolicy(check_errors, dev)
+        # overlap of the reduce-scatter with backward
+        self._pending_works: dict = {}
+        self.rs_launched_in_backward = 0  # bucket reduce-scatters started from the grad hooks
+        self._hooks = []
+        self._bucket_params = [[] for _ in L.buckets]
+        for i in range(len(self.params)):
+            for k in L.buckets_of(i):
+                self._bucket_params[k].append(i)
+        self._remaining = [len(b) for b in self._bucket_params]
+        if overlap_grad_reduce:
+            index = {id(p): i for i, p in enumerate(self.params)}
+            for p in self.params:
+                self._hooks.append(p.register_post_accumulate_grad_hook(
+                    lambda p, i=index[id(p)]: self._on_grad(i)))
+
+    # -- collectives (host-staged for gloo with CUDA tensors) -----------------------
+    def _staged(self) -> bool:
+        return self.backend == "gloo" and self.device.type == "cuda"
+
+    def _reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor, async_op: bool = False):
+        op = dist.ReduceOp.SUM
+        if self.reduce_op == "avg" and self.backend == "nccl":
+            op = dist.ReduceOp.AVG
+        if self._staged():
+            h_out = out.cpu()
+            dist.reduce_scatter_tensor(h_out, inp.cpu(), op=op, group=self.pg)
+            out.copy_(h_out)
+            work = None
+        else:
+            work = dist.reduce_scatter_tensor(out, inp, op=op, group=self.pg, async_op=async_op)
+        if self.reduce_op == "avg" and op == dist.ReduceOp.SUM:
+            if work is not None:
+                work.wait()
+                work = None
+            out.div_(self.world)
+        return work
+
+    def _all_gather(self, out: torch.Tensor, inp: torch.Tensor, async_op: bool = False):
+        if self._staged():
+            h = out.cpu()
+            dist.all_gather_into_tensor(h, inp.cpu(), group=self.pg)
+            out.copy_(h)
+            return None
+        if self.backend == "gloo":
+            inp = inp.clone()  # gloo: no aliasing of input and output
+        return dist.all_gather_into_tensor(out, inp, group=self.pg, async_op=async_op)
+
+    # -- gradients ---------------------------------------------------------------------
+    def _adopt_grad(self, i: int) -> None:
+        """Make sure parameter i's gradient lives in its flat-buffer view (a
+        user's zero_grad(set_to_none=True) or a reassignment detaches it)."""
+        p, view = self.params[i], self._grad_views[i]
+        g = p.grad
+        if g is None:
+            view.zero_()  # no gradient this step: stepped as zero (decay and momentum still apply)
+            p.grad = view
+        elif g.data_ptr() != view.data_ptr():
+            view.copy_(g.reshape(view.shape))
+            p.grad = view
+
+    def _launch_bucket_rs(self, k: int, async_op: bool):
+        s, size = self.layout.buckets[k]
+        per = size // self.world
+        so = self.layout.piece_off[k]
+        return self._reduce_scatter(self.shard_grads[so:so + per], self.flat_grads[s:s + size], async_op)
+
+    def _on_grad(self, i: int) -> None:
+        self._adopt_grad(i)
+        for k in self.layout.buckets_of(i):
+            self._remaining[k] -= 1
+            if self._remaining[k] == 0 and k not in self._pending_works:
+                self._pending_works[k] = self._launch_bucket_rs(k, async_op=True)
+                self.rs_launched_in_backward += 1
 
     # -- the three phases --------------------------------------------------------
     def reduce_scatter_grads(self) -> None:
-        op = dist.ReduceOp.SUM
-        if self.reduce_op == "avg" and dist.get_backend(self.pg) == "nccl":
-            op = dist.ReduceOp.AVG
-        dist.reduce_scatter_tensor(self.shard_grads, self.flat_grads, op=op, group=self.pg)
-        if self.reduce_op == "avg" and op == dist.ReduceOp.SUM:
-            self.shard_grads.div_(self.world)
+        if not self._hooks:
+            for i in range(len(self.params)):
+                self._adopt_grad(i)
+        for k in range(len(self.layout.buckets)):
+            if k not in self._pending_works:
+                if self._hooks:
+                    for i in self._bucket_params[k]:
+                        self._adopt_grad(i)
+                self._pending_works[k] = self._launch_bucket_rs(k, async_op=bool(self._hooks))
+        for w in self._pending_works.values():
+            if w is not None:
+                w.wait()
+        self._pending_works = {}
+        self._remaining = [len(b) for b in self._bucket_params]
+
+    def _scalars(self) -> list:
+        return [hp.scalars(self.t + 1) for hp in self.hparams]
 
     def step_shard(self) -> None:
-        grads = [self.shard_grads[s.shard_off:s.shard_off + s.length] for s in self.segments]
-        hps = [self.hparams[s.hp_index] for s in self.segments]
         if not self.states:
             return
+        grads = [self.shard_grads[s.shard_off:s.shard_off + s.length] for s in self.segments]
         if self.step_fn is not None:
+            hps = [self.hparams[s.hp_index] for s in self.segments]
             self.step_fn(self.optimizer, self.states, grads, hps)
-        else:
-            from .optim import step_many
+            return
+        from . import _lib
+        from ._errors import stream_handle
+        from .flat import StepPlan
 
-            step_many(self.optimizer, self.states, grads, hps)
+        if len(self.hparams) > _lib.FO_MAX_HPARAMS:
+            raise ValueError(f"at most {_lib.FO_MAX_HPARAMS} param groups")
+        if self._plan is None:
+            self._plan = StepPlan(self.optimizer, self.states, [s.hp_index for s in self.segments])
+            self._plan.set_grads(grads)
+        self._plan.launch(self._scalars(), self._errors.ptr, stream_handle(self.device))
 
     def all_gather_params(self) -> None:
-        dist.all_gather_into_tensor(self.flat_params, self.shard_params, group=self.pg)
+        works = []
+        for k in range(len(self.layout.buckets)):
+            s, size = self.layout.buckets[k]
+            lo, hi = self.layout.piece(k, self.rank)
+            works.append(self._all_gather(self.flat_params[s:s + size], self.flat_params[lo:hi],
+                                          async_op=len(self.layout.buckets) > 1))
+        for w in works:
+            if w is not None:
+                w.wait()
 
     @torch.no_grad()
     def step(self) -> None:
@@ -148,51 +306,57 @@ class ZeroFlashOptimizer:
         self.step_shard()
         self.all_gather_params()
         self.t += 1
+        if self._errors is not None:
+            self._errors.after_step(self.optimizer)
 
-    def zero_grad(self) -> None:
+    def raise_errors(self) -> None:
+        if self._errors is not None:
+            self._errors.raise_now(self.optimizer)
+
+    def zero_grad(self, set_to_none: bool = False) -> None:
+        """Zero the flat gradient buffer (gradients stay flat-buffer views;
+        set_to_none is accepted for torch.optim compatibility and ignored)."""
         self.flat_grads.zero_()
+        for p, v in zip(self.params, self._grad_views):
+            p.grad = v
+
+    def remove_hooks(self) -> None:
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
 
     # -- checkpoints (SURVEY.md §8e "sharded checkpoints") -----------------------
     # A tensor's state can straddle ranks.  To keep the reference layout -- one
     # FLOP v1 file per tensor with rank-1 (n,) records (checkpoint.py:73-80,
-    # :98-125) -- the shards are gathered in flat-buffer coordinates, each
-    # tensor's slices are cut out with the padding dropped, and rank 0 writes
-    # the files: byte-identical to what a single-GPU FlashState of the whole
-    # tensor writes.  Loading re-shards: every rank reads the files and keeps
-    # its own segments.
+    # :98-125) -- rank 0 gathers, a batch of tensors at a time, every rank's
+    # segments of those tensors and writes the files: byte-identical to what a
+    # single-GPU FlashState of the whole tensor writes.  Only rank 0 holds a
+    # batch (bounded by `batch_bytes`); no rank ever holds the whole state of
+    # another.  Loading re-shards: every rank reads the files of the tensors
+    # it owns segments of (and every tensor's bf16 weights).
 
-    def _local_records(self) -> dict:
-        L = self.layout
-        dev = self.flat_params.device
+    def _records(self) -> list:
         adam = self.optimizer == "adamw"
-        rho_dt = self.states[0].weights.corrections.dtype if self.states else torch.int8
-        loc = {"rho": torch.zeros(L.shard, dtype=rho_dt, device=dev),
-               "mq": torch.zeros(L.shard, dtype=torch.int8, device=dev),
-               "ms": torch.zeros(L.shard // 32, dtype=torch.float16, device=dev)}
-        if adam:
-            loc["vq"] = torch.zeros(L.shard, dtype=torch.uint8, device=dev)
-            loc["vs"] = torch.zeros(L.shard // 32, dtype=torch.float16, device=dev)
-        for seg, st in zip(self.segments, self.states):
-            a, n, ga = seg.shard_off, seg.length, seg.shard_off // 32
-            loc["rho"][a:a + n].copy_(st.weights.corrections)
-            loc["mq"][a:a + n].copy_(st.momentum.codes)
-            loc["ms"][ga:ga + st.momentum.scales.numel()].copy_(st.momentum.scales)
-            if adam:
-                loc["vq"][a:a + n].copy_(st.variance.codes)
-                loc["vs"][ga:ga + st.variance.scales.numel()].copy_(st.variance.scales)
-        return loc
+        return ["rho", "mq", "ms"] + (["vq", "vs"] if adam else [])
 
-    def _gather_records(self) -> dict:
-        """All ranks' state records in flat-buffer coordinates (collective)."""
-        out = {}
-        for k, t in self._local_records().items():
-            raw = t.view(torch.uint8)  # bytes: every backend gathers them, bit patterns untouched
-            parts = [torch.empty_like(raw) for _ in range(self.world)]
-            dist.all_gather(parts, raw, group=self.pg)
-            out[k] = torch.cat(parts).view(t.dtype)
-        return out
+    def _seg_bytes(self, seg: Segment) -> int:
+        ng = -(-seg.length // 32)
+        adam = self.optimizer == "adamw"
+        return seg.length * (3 if adam else 2) + ng * 2 * (2 if adam else 1)
 
-    def save_checkpoint(self, directory, names: Sequence[str] | None = None) -> dict | None:
+    def _pack(self, segs_states) -> torch.Tensor:
+        parts = []
+        for seg, st in segs_states:
+            parts += [st.weights.corrections.view(torch.uint8), st.momentum.codes.view(torch.uint8),
+                      st.momentum.scales.view(torch.uint8)]
+            if self.optimizer == "adamw":
+                parts += [st.variance.codes.view(torch.uint8), st.variance.scales.view(torch.uint8)]
+        if not parts:
+            return torch.zeros(0, dtype=torch.uint8, device=self.device)
+        return torch.cat([x.reshape(-1) for x in parts])
+
+    def save_checkpoint(self, directory, names: Sequence[str] | None = None,
+                        batch_bytes: int = 1 << 30) -> dict | None:
         """Collective: one FLOP v1 file per parameter plus a manifest, written
         by rank 0 (returns the manifest there, None elsewhere)."""
         import json
@@ -203,23 +367,78 @@ class ZeroFlashOptimizer:
         from .checkpoint import save_checkpoint
         from .host import HostFlashState
 
-        g = self._gather_records()
+        if self.states and self.states[0].weights.corrections.dtype != torch.int8:
+            raise ValueError("sharded checkpoints hold int8 corrections")
+        L = self.layout
+        nparams = len(self.params)
+        all_segs = [L.segments(r, self.group_of) for r in range(self.world)]
+        mine = list(zip(self.segments, self.states))
+        names = list(names) if names is not None else [f"param{i:05d}" for i in range(nparams)]
         manifest = None
         if self.rank == 0:
             os.makedirs(directory, exist_ok=True)
-            L = self.layout
-            names = list(names) if names is not None else [f"param{i:05d}" for i in range(len(self.params))]
-            host = {k: v.cpu().numpy() for k, v in g.items()}
-            lp_all = self.flat_params.view(torch.int16).cpu().numpy().view(np.uint16)
             manifest = {"format": "FLOP v1 per parameter", "optimizer": self.optimizer, "params": [], "bytes": 0}
-            for i, (p, o, n) in enumerate(zip(self.params, L.offsets, L.numels)):
-                go, ng = o // 32, -(-n // 32)
-                hs = HostFlashState(lp_all[o:o + n], host["rho"][o:o + n], host["mq"][o:o + n],
-                                    host["ms"][go:go + ng], host["vq"][o:o + n] if "vq" in host else None,
-                                    host["vs"][go:go + ng] if "vs" in host else None, self.t, 32)
-                fname = f"{i:05d}.flop"
-                manifest["bytes"] += save_checkpoint(hs, os.path.join(directory, fname), self.optimizer)
-                manifest["params"].append({"index": i, "name": names[i], "file": fname, "shape": list(p.shape)})
+        adam = self.optimizer == "adamw"
+        i0 = 0
+        while i0 < nparams:
+            # a batch of whole tensors of about batch_bytes of state
+            i1, acc = i0, 0
+            while i1 < nparams and (i1 == i0 or acc + L.numels[i1] * 3.2 <= batch_bytes):
+                acc += L.numels[i1] * 3.2
+                i1 += 1
+            sel = lambda segs: [s for s in segs if i0 <= s.param_index < i1]  # noqa: E731
+            sizes = [sum(self._seg_bytes(s) for s in sel(segs)) for segs in all_segs]
+            cap = max(sizes) if sizes else 0
+            buf = self._pack([(s, st) for s, st in mine if i0 <= s.param_index < i1])
+            send = torch.zeros(max(cap, 1), dtype=torch.uint8, device=self.device)
+            send[:buf.numel()].copy_(buf)
+            gl = [torch.empty_like(send) for _ in range(self.world)] if self.rank == 0 else None
+            if self._staged():
+                h = send.cpu()
+                hl = [torch.empty_like(h) for _ in range(self.world)] if self.rank == 0 else None
+                dist.gather(h, hl, dst=0, group=self.pg)
+                gl = hl
+            else:
+                dist.gather(send, gl, dst=0, group=self.pg)
+            if self.rank == 0:
+                lp_all = self.flat_params.view(torch.int16)
+                arrays = {}
+                for i in range(i0, i1):
+                    n = L.numels[i]
+                    ng = -(-n // 32)
+                    arrays[i] = {"rho": np.zeros(n, np.int8), "mq": np.zeros(n, np.int8),
+                                 "ms": np.zeros(ng, np.float16), "vq": np.zeros(n, np.uint8) if adam else None,
+                                 "vs": np.zeros(ng, np.float16) if adam else None}
+                for r in range(self.world):
+                    raw = gl[r].cpu().numpy()
+                    pos = 0
+                    for s in sel(all_segs[r]):
+                        a, m, ga, ng = s.tensor_off, s.length, s.tensor_off // 32, -(-s.length // 32)
+                        d = arrays[s.param_index]
+
+                        def take(nbytes, dt):
+                            nonlocal pos
+                            out = raw[pos:pos + nbytes].view(dt)
+                            pos += nbytes
+                            return out
+
+                        d["rho"][a:a + m] = take(m, np.int8)
+                        d["mq"][a:a + m] = take(m, np.int8)
+                        d["ms"][ga:ga + ng] = take(2 * ng, np.float16)
+                        if adam:
+                            d["vq"][a:a + m] = take(m, np.uint8)
+                            d["vs"][ga:ga + ng] = take(2 * ng, np.float16)
+                for i in range(i0, i1):
+                    o, n = L.offsets[i], L.numels[i]
+                    lp = lp_all[o:o + n].cpu().numpy().view(np.uint16)
+                    d = arrays[i]
+                    hs = HostFlashState(lp, d["rho"], d["mq"], d["ms"], d["vq"], d["vs"], self.t, 32)
+                    fname = f"{i:05d}.flop"
+                    manifest["bytes"] += save_checkpoint(hs, os.path.join(directory, fname), self.optimizer)
+                    manifest["params"].append({"index": i, "name": names[i], "file": fname,
+                                               "shape": list(self.params[i].shape)})
+            i0 = i1
+        if self.rank == 0:
             with open(os.path.join(directory, "manifest.json"), "w") as f:
                 json.dump(manifest, f, indent=1)
         dist.barrier(group=self.pg)
@@ -231,6 +450,8 @@ class ZeroFlashOptimizer:
         files written by save_checkpoint (or by single-GPU save_optimizer)."""
         import json
         import os
+
+        import numpy as np
 
         from .checkpoint import CheckpointError, load_checkpoint
 
@@ -251,6 +472,9 @@ class ZeroFlashOptimizer:
             o, n = L.offsets[i], L.numels[i]
             if hs.length != n:
                 raise CheckpointError(f"parameter {i}: checkpoint has {hs.length} elements, model {n}")
+            if hs.rho.dtype != np.int8 or hs.group_size != 32:
+                raise CheckpointError(f"parameter {i}: the sharded optimizer holds int8 corrections with "
+                                      f"groups of 32 (file: {hs.rho.dtype}, G={hs.group_size})")
             step = hs.t
             self.flat_params[o:o + n].copy_(torch.from_numpy(hs.lp.view("int16")).to(dev).view(torch.bfloat16))
             for seg, st in by_param.get(i, []):

@@ -58,7 +58,17 @@ def _grads(step, seed=100):
     return [(torch.randn(n, generator=g) * 1e-3).to(torch.bfloat16) for n in SIZES]
 
 
-def _worker(rank, world, port, opt, q):
+def _worker(rank, world, port, opt, q, zkw=None, mode="assign"):
+    try:
+        _worker_body(rank, world, port, opt, q, zkw, mode)
+    except BaseException:  # report instead of leaving the parent waiting
+        import traceback
+
+        q.put((rank, "error", traceback.format_exc()))
+        raise
+
+
+def _worker_body(rank, world, port, opt, q, zkw, mode):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -70,16 +80,35 @@ def _worker(rank, world, port, opt, q):
     from paper_2602_23349_b200.zero import ZeroFlashOptimizer
 
     params = _init_params()
+    if mode != "assign":
+        params = [p.requires_grad_() for p in params]
     hp = {"adamw": [FO.AdamHyperParams(lr=1e-3, beta2=0.95, weight_decay=0.1), FO.AdamHyperParams(lr=1e-3)],
           "sgd": [FO.SgdHyperParams(lr=0.1, weight_decay=1e-4), FO.SgdHyperParams(lr=0.1)],
           "lion": [FO.LionHyperParams(lr=1e-4, weight_decay=0.1), FO.LionHyperParams(lr=1e-4)]}[opt]
-    zo = ZeroFlashOptimizer(params, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum")
+    zo = ZeroFlashOptimizer(params, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum",
+                            **(zkw or {}))
     for s in range(STEPS):
-        zo.zero_grad()
-        if rank == 0:
-            for p, g in zip(params, _grads(s)):
-                p.grad.copy_(g)
+        if mode == "assign":
+            zo.zero_grad()
+            if rank == 0:
+                for p, g in zip(params, _grads(s)):
+                    p.grad.copy_(g)
+        else:
+            # a real backward: rank 0's loss has gradient exactly g, rank 1's is
+            # exactly zero; with mode "none" the user sets grads to None first
+            # (torch's default zero_grad), which detaches them from the flat buffer
+            if mode == "none":
+                for p in params:
+                    p.grad = None
+            else:
+                zo.zero_grad()
+            gs = _grads(s)
+            loss = sum((p * (g if rank == 0 else torch.zeros_like(g))).sum() for p, g in zip(params, gs))
+            loss.backward()
         zo.step()
+    if zkw and zkw.get("overlap_grad_reduce"):
+        # every bucket's reduce-scatter was started inside backward
+        assert zo.rs_launched_in_backward == STEPS * len(zo.layout.buckets) > STEPS, zo.rs_launched_in_backward
     full = [p.detach().clone() for p in params]
     shard_state = [(seg.param_index, seg.tensor_off, seg.length,
                     {"rho": st.weights.corrections.numpy().copy(), "m": st.momentum.codes.numpy().copy(),
@@ -89,15 +118,35 @@ def _worker(rank, world, port, opt, q):
     dist.destroy_process_group()
 
 
+LAYOUTS = {
+    "one-bucket": (None, "assign"),
+    "buckets": ({"bucket_elems": 2048}, "assign"),
+    "overlap-hooks": ({"bucket_elems": 4096, "overlap_grad_reduce": True}, "backward"),
+    "overlap-set-to-none": ({"bucket_elems": 4096, "overlap_grad_reduce": True}, "none"),
+    "no-hooks-set-to-none": ({"bucket_elems": 8192}, "none"),
+}
+
+
+@pytest.mark.parametrize("layout", list(LAYOUTS))
 @pytest.mark.parametrize("opt", ["adamw", "sgd", "lion"])
-def test_zero1_matches_unsharded_oracle(opt, oracle_mod):
+def test_zero1_matches_unsharded_oracle(opt, layout, oracle_mod):
+    """Bucketed ownership (rank r owns piece r of every bucket), the
+    reduce-scatter launched per bucket from post-accumulate-grad hooks while
+    backward runs, and gradients detached by set_to_none: all bitwise equal to
+    the unsharded oracle."""
+    if layout != "one-bucket" and opt != "adamw":
+        pytest.skip("layouts are optimizer-independent; covered with adamw")
+    zkw, mode = LAYOUTS[layout]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, opt, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, opt, q, zkw, mode)) for r in range(2)]
     for p in procs:
         p.start()
-    results = dict((r, (f, s)) for r, f, s in (q.get(timeout=300) for _ in range(2)))
+    got = [q.get(timeout=300) for _ in range(2)]
+    errs = [x[2] for x in got if isinstance(x[1], str)]
+    assert not errs, errs[0]
+    results = dict((r, (f, s)) for r, f, s in got)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -156,17 +205,19 @@ def _worker_ckpt(rank, world, port, opt, q, directory):
           "sgd": [FO.SgdHyperParams(lr=0.1, weight_decay=1e-4), FO.SgdHyperParams(lr=0.1)],
           "lion": [FO.LionHyperParams(lr=1e-4, weight_decay=0.1), FO.LionHyperParams(lr=1e-4)]}[opt]
     params = _init_params()
-    zo = ZeroFlashOptimizer(params, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum")
+    zo = ZeroFlashOptimizer(params, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum",
+                            bucket_elems=4096)
     for s in range(STEPS):
         zo.zero_grad()
         if rank == 0:
             for p, g in zip(params, _grads(s)):
                 p.grad.copy_(g)
         zo.step()
-    zo.save_checkpoint(directory)
+    zo.save_checkpoint(directory, batch_bytes=20_000)  # several gather batches
     # restore into a fresh optimizer over zeroed parameters
     fresh = [torch.zeros_like(p) for p in _init_params()]
-    z2 = ZeroFlashOptimizer(fresh, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum")
+    z2 = ZeroFlashOptimizer(fresh, opt, hp, group_of=[0, 1, 0, 1, 1], step_fn=_oracle_step_fn, reduce_op="sum",
+                            bucket_elems=4096)
     z2.load_checkpoint(directory)
     same = torch.equal(zo.flat_params.view(torch.int16), z2.flat_params.view(torch.int16)) and z2.t == zo.t
     for a, b in zip(zo.states, z2.states):
