@@ -182,7 +182,8 @@ int fo_dequantize_variance(const uint8_t *codes, const uint16_t *scales, int64_t
  * f32 bit patterns [begin, begin+count); 1: reciprocal of every fp16 value;
  * 2/3/4: hash-sampled quotients (per-element, per-group-scale and
  * bias-correction divisors); 6: the fused tile's integer reconstruct over
- * every (bf16 code, rho).  d_out[0] += mismatches, d_out[1] = min failing
+ * every (bf16 code, rho); 7: the wide-range sqrt over f32 bit patterns
+ * [begin, begin+count) below 2^64.  d_out[0] += mismatches, d_out[1] = min failing
  * index (initialise to 0 and UINT64_MAX); mode 5 writes raw sqrt results to
  * d_out[2..] (debug). */
 int fo_selftest(int mode, uint64_t begin, uint64_t count, uint64_t *d_out, void *stream);

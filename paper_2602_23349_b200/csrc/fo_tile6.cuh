@@ -27,6 +27,11 @@
 #ifndef FO_VG
 #define FO_VG 1
 #endif
+// Steady state (f32 bias corrections == 1): the variance root is taken with
+// fast::sqrt_rn2_wide, exact for every v < 2^64, so the v operand guard goes.
+#ifndef FO_SQRT_WIDE
+#define FO_SQRT_WIDE 1
+#endif
 
 struct Luts6 {
   int r[256];    // R(rho) by byte, signed; 0 for the invalid code -128 (caught by the rho guard)
@@ -389,15 +394,16 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       const float2 vp2 = fma2(r2, r2, Z);
       m2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
       const float2 v2 = add2(fma2(dup(h.b2), vp2, Z), fma2(dup(h.omb2), fma2(g2, g2, Z), Z));
+      constexpr bool WIDE_ROOT = FO_SQRT_WIDE && (BC & 2) && !SAFE;
       if (!SAFE && VG) {
         mlo = __vimin3_u32(mlo, (__float_as_uint(m2.x) << 1) - 2u, (__float_as_uint(m2.y) << 1) - 2u);
-        vlo = __vimin3_u32(vlo, (__float_as_uint(v2.x) << 1) - 2u, (__float_as_uint(v2.y) << 1) - 2u);
+        if (!WIDE_ROOT) vlo = __vimin3_u32(vlo, (__float_as_uint(v2.x) << 1) - 2u, (__float_as_uint(v2.y) << 1) - 2u);
       }
       const float2 mh = (BC & 1) ? m2 : quot_y<SAFE>(m2, h.bc1, h.rbc1);
       float2 rt2;  // RN(sqrt(v)), also quantize.py:145
       float2 den;
       if (BC & 2) {
-        rt2 = root2<SAFE>(v2);
+        rt2 = WIDE_ROOT ? sqrt_rn2_wide(v2) : root2<SAFE>(v2);
         den = add2(rt2, dup(h.eps));
       } else {
         rt2 = root2<SAFE>(v2);
@@ -464,6 +470,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     bad |= !(tmin >= 0x1p-113f) || !(tmax < 0x1.FFp127f);
     if (VG) {
       if (ADAM) bad |= mlo < 2u * 0x15800000u - 2u || vlo < 2u * 0x10800000u - 2u;  // 0 < |m| < 2^-84, 0 < v < 2^-94
+      // (vlo stays at its initial maximum when the wide root needs no v guard)
     } else if (sizeof(GradT) == 2) {
       bad |= __vcmpltu2(gmin, 0x2DFF2DFFu) != 0;
     } else {

@@ -32,6 +32,13 @@ def test_sqrt_exhaustive(cuda_dev):
     assert bad == 0, f"{bad} mismatches, first at bits {first:#x}"
 
 
+def test_wide_sqrt_exhaustive(cuda_dev):
+    """sqrt_rn2_wide == sqrt.rn for every f32 in [0, 2^64), subnormals included
+    (the steady-state AdamW tile's variance root, no operand guard)."""
+    bad, first = _run(7, 0, 0x5F800000)
+    assert bad == 0, f"{bad} mismatches, first at bits {first:#x}"
+
+
 def test_reciprocal_of_every_fp16_scale(cuda_dev):
     bad, first = _run(1, 0, 0x7C00)
     assert bad == 0, f"first failing fp16 bits {first:#x}"

@@ -31,7 +31,7 @@ import torch  # noqa: E402
 HP = dict(lr=6e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
 
 
-def make_model(dtype):
+def make_model(dtype, checkpointing: bool = False):
     from transformers import GPT2Config, GPT2LMHeadModel
 
     cfg = GPT2Config(n_layer=24, n_embd=1024, n_head=16, n_positions=1024, vocab_size=50257,
@@ -39,6 +39,8 @@ def make_model(dtype):
     torch.manual_seed(0)
     m = GPT2LMHeadModel(cfg)
     m.config._attn_implementation = "sdpa"
+    if checkpointing:
+        m.gradient_checkpointing_enable()
     return m.to(device="cuda", dtype=dtype)
 
 
@@ -49,7 +51,7 @@ def run_mode(mode: str, args) -> dict:
     torch.cuda.empty_cache()
     torch.cuda.reset_peak_memory_stats()
     fp32_master = mode == "torch_adamw_fp32"
-    model = make_model(torch.float32 if fp32_master else torch.bfloat16)
+    model = make_model(torch.float32 if fp32_master else torch.bfloat16, args.checkpointing)
     params = [p for p in model.parameters()]
     n_params = sum(p.numel() for p in params)
     release = None
@@ -58,16 +60,20 @@ def run_mode(mode: str, args) -> dict:
     else:
         opt = FlashAdamW(params, check_errors=False, **HP)
         if mode == "flash_release":
-            release = GradientRelease(opt)
+            release = GradientRelease(opt, timing=True)
     g = torch.Generator(device="cuda").manual_seed(1)
     batches = [torch.randint(0, 50257, (args.batch, args.seq), device="cuda", generator=g) for _ in range(4)]
     opt_ev = []
+    boundary = []  # bytes allocated when backward has returned (the optimizer boundary)
 
     def step(i):
         x = batches[i % len(batches)]
         with torch.autocast("cuda", dtype=torch.bfloat16, enabled=fp32_master):
             loss = model(input_ids=x, labels=x).loss
         loss.backward()
+        if i == 0 or len(boundary) < 2:
+            torch.cuda.synchronize()
+            boundary.append(torch.cuda.memory_allocated())
         if release is None:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
@@ -81,6 +87,9 @@ def run_mode(mode: str, args) -> dict:
         step(i)
     torch.cuda.synchronize()
     opt_ev.clear()
+    if release is not None:
+        release.side_stream_ms()  # drop the warm-up launches
+    torch.cuda.reset_peak_memory_stats()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
     for i in range(args.steps):
@@ -93,6 +102,13 @@ def run_mode(mode: str, args) -> dict:
     elif mode != "torch_adamw_fp32":
         opt.raise_errors()
     opt_ms = sum(a.elapsed_time(b) for a, b in opt_ev) / len(opt_ev) if opt_ev else None
+    peak = torch.cuda.max_memory_allocated()
+    release_info = None
+    if release is not None:
+        opt_ms = release.side_stream_ms() / args.steps
+        release_info = {"launch_calls_per_step": release.launch_calls / (args.warmup + args.steps),
+                        "bucket_elems": release.bucket_elems,
+                        "optimizer_ms_is": "side-stream device time of the fused launches (overlaps backward)"}
     # optimizer step alone, back to back on resident gradients: device time per
     # step (host enqueue cost overlaps), and the host cost of one step() call
     iso = None
@@ -120,17 +136,24 @@ def run_mode(mode: str, args) -> dict:
             if isinstance(v, torch.Tensor):
                 state_bytes += v.numel() * v.element_size()
     weight_bytes = sum(p.numel() * p.element_size() for p in params)
+    # bytes held at the optimizer boundary beyond weights + optimizer state:
+    # the gradients (2 B/param in bf16) in deferred mode, ~0 with release
     out = {
         "config": "gpt2_medium_train", "mode": mode, "params": n_params, "batch": args.batch, "seq": args.seq,
         "tokens_per_s": args.batch * args.seq / (ms * 1e-3), "ms_per_step": ms,
         "optimizer_step_ms": opt_ms,
         "optimizer_gparams_per_s": (n_params / (opt_ms * 1e-3) / 1e9) if opt_ms else None,
         "optimizer_step_back_to_back": iso,
-        "peak_mem_gib": torch.cuda.max_memory_allocated() / 2**30,
+        "peak_mem_gib": peak / 2**30,
+        "allocated_at_optimizer_boundary_gib": boundary[-1] / 2**30,
+        "boundary_minus_weights_and_state_bytes_per_param": None,
+        "activation": "checkpointed" if args.checkpointing else "stored",
+        "release": release_info,
         "weights_plus_state_bytes_per_param": (weight_bytes + state_bytes) / n_params,
         "final_loss": float(loss.item()),
         "data": "synthetic tokens, random init",
     }
+    out["boundary_minus_weights_and_state_bytes_per_param"] = (boundary[-1] - weight_bytes - state_bytes) / n_params
     if mode == "flash":
         out["checkpoint"] = checkpoint_roundtrip(opt, params)
     if release is not None:
@@ -182,6 +205,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--modes", default="flash,flash_release,torch_adamw_fp32")
+    ap.add_argument("--checkpointing", action="store_true",
+                    help="activation checkpointing (small activations, so gradients matter for the peak)")
     args = ap.parse_args()
     for mode in args.modes.split(","):
         print(json.dumps(run_mode(mode, args)), flush=True)
