@@ -657,15 +657,22 @@ def e2e_leg(args, states, grads, opt, hp, world, n_local, n_all, dev, reduce_):
 
 
 def traffic_for(args, n_local: int):
+    """ncu DRAM bytes (read + write) per launch for this config, scaled from
+    the bytes per parameter of a --set full capture (profiles/ncu_traffic.json:
+    the headline launch itself for the Llama list)."""
     if args.traffic is not None:
         return args.traffic, "--traffic"
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        src = d.get("source", "profiles/ncu_traffic.json")
-        return d["bytes_per_param"] * n_local / 1e9, f"{src} (ncu dram bytes per param x params)"
+        if args.config == "llama31_8b" and args.optimizer == "adamw":
+            return d["bytes_per_param"] * n_local / 1e9, d["source"]
+        key = f"{args.config}_{args.optimizer}"
+        if key in d.get("other_lists", {}):
+            return d["other_lists"][key] * n_local / 1e9, f"profiles/ncu_traffic.json other_lists[{key}]"
     except Exception:
-        return None, None
+        pass
+    return None, None
 
 
 # ---------------------------------------------------------------------------
