@@ -32,6 +32,16 @@
 #ifndef FO_SQRT_WIDE
 #define FO_SQRT_WIDE 1
 #endif
+// Split code from a K * 2^-13 made by one LOP3 (1 instead of 2 integer ops
+// per element); 0: K = 127 * 2^-ell by LOP3 + IADD3.
+#ifndef FO_SPLIT_K13
+#define FO_SPLIT_K13 1
+#endif
+// Steady-state AdamW keeps the variance roots scaled by 2^30 (one FMUL2 per
+// pair fewer); 0: unscaled roots.
+#ifndef FO_ROOT_SCALED
+#define FO_ROOT_SCALED 1
+#endif
 
 struct Luts6 {
   int r[256];    // R(rho) by byte, signed; 0 for the invalid code -128 (caught by the rho guard)
@@ -51,6 +61,14 @@ __device__ __forceinline__ void init_luts6(Luts6& L) {
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   uint32_t r;
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// (~t & 0x7F800000) | 0x007E0000 as one LOP3 (left to itself ptxas emits a
+// mask and an XOR): K * 2^-13 of the split, see compute_tile6.
+__device__ __forceinline__ uint32_t k13_bits(uint32_t t) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xAE;" : "=r"(r) : "r"(t), "r"(0x7F800000u), "r"(0x007E0000u));
   return r;
 }
 
@@ -285,6 +303,11 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   const float2 Z = dup(negzero);
   const int64_t n = T.n;
   const int64_t e0 = base + (int64_t)lane * E;
+  // steady-state AdamW keeps the variance roots scaled by 2^30 (RSCALED):
+  // every use of them is a max, a quotient by the group scale or the sum
+  // with eps, and all three take the exact power-of-two scaling for free
+  constexpr bool RSCALED = FO_ROOT_SCALED && ADAM && FO_SQRT_WIDE && (BC & 2) && !SAFE;
+  constexpr float RS = RSCALED ? 0x1p30f : 1.0f;
 #ifdef FO_COPY_ONLY
   // bandwidth/power experiment: same loads and stores, no arithmetic
   if (full) {
@@ -403,8 +426,15 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       float2 rt2;  // RN(sqrt(v)), also quantize.py:145
       float2 den;
       if (BC & 2) {
-        rt2 = WIDE_ROOT ? sqrt_rn2_wide(v2) : root2<SAFE>(v2);
-        den = add2(rt2, dup(h.eps));
+        if (RSCALED) {
+          // root * 2^30 (sqrt_rn2_wide without its final exact * 2^-30); the
+          // 2^-30 is folded into den's FFMA2 and the variance epilogue
+          rt2 = sqrt_rn2(mul2(v2, dup(0x1p60f)));
+          den = fma2(rt2, dup(0x1p-30f), dup(h.eps));  // RN(root + eps): root'*2^-30 is exact
+        } else {
+          rt2 = WIDE_ROOT ? sqrt_rn2_wide(v2) : root2<SAFE>(v2);
+          den = add2(rt2, dup(h.eps));
+        }
       } else {
         rt2 = root2<SAFE>(v2);
         den = add2(root2<SAFE>(quot_y<SAFE>(v2, h.bc2, h.rbc2)), dup(h.eps));
@@ -445,6 +475,18 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       cw[k] = *reinterpret_cast<uint32_t*>(&c2);
       const float2 lp2 = make_float2(__uint_as_float(cw[k] << 16), __uint_as_float(cw[k] & 0xFFFF0000u));
       const float2 e2 = add2(tn2, neg2(lp2));  // exact residual
+#if FO_SPLIT_K13
+      // K = 127 * 2^-ell with ell = expf(theta) - 135 (the binade-bottom rule
+      // is implied by theta's own exponent).  K * 2^-13 = (127/64) *
+      // 2^(128 - expf) has exponent field 255 - expf, i.e. the complement of
+      // theta's: ONE LOP3 per element, normal for every expf in [1, 254].
+      const float2 k2 = make_float2(__uint_as_float(k13_bits(__float_as_uint(tn2.x))),
+                                    __uint_as_float(k13_bits(__float_as_uint(tn2.y))));
+      // e*K*2^-13 is exact (<= 24 significant bits, |.| < 2^-6) and 1536 has
+      // ulp 2^-13, so RN(e*K*2^-13 + 1536) = 1536 + rint(e*K) * 2^-13
+      // (ties-to-even): the code sits in the low mantissa bits.
+      const float2 q2 = fma2(e2, k2, dup(1536.0f));
+#else
       // K = 127 * 2^-ell with ell = expf(theta) - 135: the binade-bottom rule
       // is implied by theta's own exponent; valid for expf(theta) in [14, 254].
       const float2 k2 = make_float2(__uint_as_float(0x867E0000u - (__float_as_uint(tn2.x) & 0x7F800000u)),
@@ -452,6 +494,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       // e*K is exact (<= 24 significant bits), so adding 1.5*2^23 in the same
       // FFMA2 leaves rint(e*K) (ties-to-even) in the low mantissa bits.
       const float2 q2 = fma2(e2, k2, dup(12582912.0f));
+#endif
       pr = prmt(__float_as_uint(q2.x), __float_as_uint(q2.y), 0x0040u);
     }
     if (k & 1) ro[k >> 1] = prmt(ro[k >> 1], pr, 0x5410u);
@@ -514,11 +557,13 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     for (int j = 0; j < E; j += 2) rmax = maxnan3(rmax, root[j], root[j + 1]);
 #pragma unroll
     for (int o = 1; o < LPG; o <<= 1) rmax = maxnan(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-    bad |= !(rmax <= 65504.0f);
-    new_vsb = (uint32_t)__half_as_ushort(__float2half_ru(rmax));
+    bad |= !(rmax <= 65504.0f * RS);
+    new_vsb = (uint32_t)__half_as_ushort(__float2half_ru(RSCALED ? __fmul_rn(rmax, 1.0f / RS) : rmax));
     const float s = half_bits_to_float(new_vsb);
-    const float den = (s == 0.0f) ? 1.0f : s;
-    const float y = rcp_rn_normal(den);
+    // RSCALED: RN(root'/(s*2^30)) with y = RN(1/s)*2^-30 is the same
+    // Markstein quotient as RN(root/s) with every intermediate scaled exactly
+    const float den = RSCALED ? __fmul_rn((s == 0.0f) ? 1.0f : s, RS) : ((s == 0.0f) ? 1.0f : s);
+    const float y = RSCALED ? __fmul_rn(rcp_rn_normal((s == 0.0f) ? 1.0f : s), 1.0f / RS) : rcp_rn_normal(den);
 #pragma unroll
     for (int j = 0; j < E; j += 2) {
       const float2 vn = quot_y<SAFE>(make_float2(root[j], root[j + 1]), den, y);  // RN(r/s)
