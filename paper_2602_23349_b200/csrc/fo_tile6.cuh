@@ -72,6 +72,13 @@ __device__ __forceinline__ uint32_t k13_bits(uint32_t t) {
   return r;
 }
 
+// (~t & 0x7F800000) | 0x007FFE00: K * 2^-21 of the int16 split.
+__device__ __forceinline__ uint32_t k16_bits(uint32_t t) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xAE;" : "=r"(r) : "r"(t), "r"(0x7F800000u), "r"(0x007FFE00u));
+  return r;
+}
+
 // Compact LUTs (3 KB): index = code byte, one PRMT + one LEA per lookup.
 struct NarrowLut {
   const Luts6& L;
@@ -132,53 +139,28 @@ __device__ __forceinline__ WideLut init_wide_lut(uint8_t* dsm, Luts6& Ls) {
                  WIDE_LUT_ADDR | (4u * (2 * WIDE_COPIES + c))};
 }
 
-template <typename GradT>
+// RB: bytes per correction code (1: int8, N = 127; 2: int16, N = 32767).
+template <int NCORR>
+struct Corr {
+  static constexpr int RB = NCORR == 127 ? 1 : 2;
+  typedef typename std::conditional<NCORR == 127, int8_t, int16_t>::type T;
+};
+
+template <typename GradT, int NCORR = 127>
 struct TileIn6 {
   static constexpr int E = FEPL, NW = FEPL / 2, NB = FEPL / 4;
   static constexpr int NG = sizeof(GradT) == 2 ? NW : E;  // grad words
-  uint32_t lw[NW], rw[NB], mw[NB], vw[NB], gw[NG];
+  static constexpr int NR = NB * Corr<NCORR>::RB;        // correction words
+  uint32_t lw[NW], rw[NR], mw[NB], vw[NB], gw[NG];
   uint32_t msb, vsb;
 };
 
-template <int OPT, typename GradT>
-__device__ __forceinline__ void load6_smem(const uint8_t* lp, const uint8_t* g, const uint8_t* rho, const uint8_t* mq,
-                                           const uint8_t* vq, const uint16_t* ms, const uint16_t* vs, int lane,
-                                           TileIn6<GradT>& in) {
-  constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
-  constexpr int E = FEPL, NW = E / 2, NB = E / 4, NG = TileIn6<GradT>::NG;
-  const int e = lane * E;
-#pragma unroll
-  for (int c = 0; c < NW / 4; ++c) {
-    const uint4 a = *reinterpret_cast<const uint4*>(lp + 2 * e + 16 * c);
-    in.lw[4 * c] = a.x; in.lw[4 * c + 1] = a.y; in.lw[4 * c + 2] = a.z; in.lw[4 * c + 3] = a.w;
-  }
-#pragma unroll
-  for (int c = 0; c < NG / 4; ++c) {
-    const uint4 a = *reinterpret_cast<const uint4*>(g + sizeof(GradT) * e + 16 * c);
-    in.gw[4 * c] = a.x; in.gw[4 * c + 1] = a.y; in.gw[4 * c + 2] = a.z; in.gw[4 * c + 3] = a.w;
-  }
-  auto bytes = [&](const uint8_t* src, uint32_t* wd) {
-    if (NB == 4) {
-      const uint4 a = *reinterpret_cast<const uint4*>(src + e);
-      wd[0] = a.x; wd[1] = a.y; wd[2] = a.z; wd[3] = a.w;
-    } else {
-      const uint2 a = *reinterpret_cast<const uint2*>(src + e);
-      wd[0] = a.x; wd[1] = a.y;
-    }
-  };
-  bytes(rho, in.rw);
-  bytes(mq, in.mw);
-  if (ADAM) bytes(vq, in.vw);
-  in.msb = ms[e / GROUP];
-  in.vsb = ADAM ? vs[e / GROUP] : 0u;
-}
-
 // Partial (or unaligned) tile straight from global memory; elements past n
 // read as zero state with zero gradient.
-template <int OPT, typename GradT>
-__device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int lane, TileIn6<GradT>& in) {
+template <int OPT, typename GradT, int NCORR = 127>
+__device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int lane, TileIn6<GradT, NCORR>& in) {
   constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
-  constexpr int E = FEPL, NW = E / 2, NB = E / 4, NG = TileIn6<GradT>::NG;
+  constexpr int E = FEPL, NW = E / 2, NB = E / 4, NG = TileIn6<GradT, NCORR>::NG, NR = TileIn6<GradT, NCORR>::NR;
   const int64_t n = T.n;
   const int64_t e0 = base + (int64_t)lane * E;
   // elements past n: weight 1.0 (0x3F80), zero correction, codes, scales
@@ -190,13 +172,16 @@ __device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int la
 #pragma unroll
   for (int q = 0; q < NG; ++q) in.gw[q] = 0;
 #pragma unroll
-  for (int q = 0; q < NB; ++q) in.rw[q] = in.mw[q] = in.vw[q] = 0;
+  for (int q = 0; q < NB; ++q) in.mw[q] = in.vw[q] = 0;
+#pragma unroll
+  for (int q = 0; q < NR; ++q) in.rw[q] = 0;
 #pragma unroll
   for (int j = 0; j < E; ++j) {
     const int64_t i = e0 + j;
     if (i < n) {
       in.lw[j >> 1] = (in.lw[j >> 1] & (0xFFFF0000u >> (16 * (j & 1)))) | ((uint32_t)T.lp[i] << (16 * (j & 1)));
-      in.rw[j >> 2] |= (uint32_t)(uint8_t)T.rho[i] << (8 * (j & 3));
+      if (NCORR == 127) in.rw[j >> 2] |= (uint32_t)(uint8_t)T.rho[i] << (8 * (j & 3));
+      else in.rw[j >> 1] |= (uint32_t)reinterpret_cast<const uint16_t*>(T.rho)[i] << (16 * (j & 1));
       in.mw[j >> 2] |= (uint32_t)(uint8_t)T.mq[i] << (8 * (j & 3));
       if (ADAM) in.vw[j >> 2] |= (uint32_t)T.vq[i] << (8 * (j & 3));
       if (sizeof(GradT) == 2)
@@ -211,9 +196,9 @@ __device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int la
 
 // Sources of one lane's 16 elements, read half (8 elements) at a time so
 // only half of the packed inputs is live at once.
-template <int OPT, typename GradT>
+template <int OPT, typename GradT, int NCORR = 127>
 struct SmemSrc {  // a full tile in the stage ring (read in place)
-  static constexpr int NGH = TileIn6<GradT>::NG / 2;
+  static constexpr int NGH = TileIn6<GradT, NCORR>::NG / 2;
   const uint8_t *lp, *g, *rho, *mq, *vq;
   uint32_t msb, vsb;
   uint32_t release_bar;  // mbarrier to arrive on once the second half is read (0: none)
@@ -226,8 +211,13 @@ struct SmemSrc {  // a full tile in the stage ring (read in place)
       const uint4 b = *reinterpret_cast<const uint4*>(g + 4 * NGH * h + 16 * c);
       gw[4 * c] = b.x; gw[4 * c + 1] = b.y; gw[4 * c + 2] = b.z; gw[4 * c + 3] = b.w;
     }
-    const uint2 r = *reinterpret_cast<const uint2*>(rho + 8 * h);
-    rw[0] = r.x; rw[1] = r.y;
+    if (NCORR == 127) {
+      const uint2 r = *reinterpret_cast<const uint2*>(rho + 8 * h);
+      rw[0] = r.x; rw[1] = r.y;
+    } else {
+      const uint4 r = *reinterpret_cast<const uint4*>(rho + 16 * h);
+      rw[0] = r.x; rw[1] = r.y; rw[2] = r.z; rw[3] = r.w;
+    }
     const uint2 m = *reinterpret_cast<const uint2*>(mq + 8 * h);
     mw[0] = m.x; mw[1] = m.y;
     if (OPT == FO_OPT_ADAMW) {
@@ -244,10 +234,11 @@ struct SmemSrc {  // a full tile in the stage ring (read in place)
   }
 };
 
-template <typename GradT>
+template <typename GradT, int NCORR = 127>
 struct RegSrc {  // a partial tile already gathered into registers
-  static constexpr int NGH = TileIn6<GradT>::NG / 2;
-  const TileIn6<GradT>& in;
+  static constexpr int NGH = TileIn6<GradT, NCORR>::NG / 2;
+  static constexpr int NRH = TileIn6<GradT, NCORR>::NR / 2;
+  const TileIn6<GradT, NCORR>& in;
   uint32_t msb, vsb;
   __device__ __forceinline__ void half(int h, uint32_t* lw, uint32_t* gw, uint32_t* rw, uint32_t* mw,
                                        uint32_t* vw) const {
@@ -256,8 +247,9 @@ struct RegSrc {  // a partial tile already gathered into registers
 #pragma unroll
     for (int q = 0; q < NGH; ++q) gw[q] = in.gw[NGH * h + q];
 #pragma unroll
+    for (int q = 0; q < NRH; ++q) rw[q] = in.rw[NRH * h + q];
+#pragma unroll
     for (int q = 0; q < 2; ++q) {
-      rw[q] = in.rw[2 * h + q];
       mw[q] = in.mw[2 * h + q];
       vw[q] = in.vw[2 * h + q];
     }
@@ -290,7 +282,8 @@ __device__ __forceinline__ float2 root2(float2 x) {
 // square root and the exact reconstruct / split of fo_math.cuh, so only the
 // reference's error conditions (non-finite values, rho = -128, scale
 // overflow) remain; those go to process_tile_exact, which reports them.
-template <int OPT, typename GradT, int BC, class Src, class Lut, bool SAFE = false>
+template <int OPT, typename GradT, int BC, class Src, class Lut, bool SAFE = false, int NCORR = 127,
+          bool LINEAR = false>
 __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h, int64_t base, int lane,
                                               uint32_t& err, const Lut& L, float negzero, uint32_t* fix,
                                               uint32_t fix_idx, bool full, const Src& in) {
@@ -307,10 +300,18 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   // every use of them is a max, a quotient by the group scale or the sum
   // with eps, and all three take the exact power-of-two scaling for free
   constexpr bool RSCALED = FO_ROOT_SCALED && ADAM && FO_SQRT_WIDE && (BC & 2) && !SAFE;
-  constexpr float RS = RSCALED ? 0x1p30f : 1.0f;
+  // ... which the variance epilogue sees only when it quantises the roots
+  // (companded); the linear ablation quantises v itself
+  constexpr bool QSCALED = RSCALED && !LINEAR;
+  constexpr float RS = QSCALED ? 0x1p30f : 1.0f;
+  // int16 corrections (formats.py:94-95): no R(rho) table; the reconstruct
+  // and the split compute with N = 32767 (see below)
+  constexpr bool C16 = NCORR != 127;
+  static_assert(!SAFE || (!C16 && !LINEAR), "the SAFE tile is the int8 / companded layout's");
+  constexpr int RB = Corr<NCORR>::RB;
 #ifdef FO_COPY_ONLY
   // bandwidth/power experiment: same loads and stores, no arithmetic
-  if (full) {
+  if (!C16 && full) {
     uint32_t hl[4], hg[TileIn6<GradT>::NG / 2], hr[2], hm[2], hv[2], a[8], b[4], c[4], d[4];
     for (int hh = 0; hh < 2; ++hh) {
       in.half(hh, hl, hg, hr, hm, hv);
@@ -357,10 +358,10 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   const float msf = half_bits_to_float(in.msb);
   const float vsf = half_bits_to_float(in.vsb);
   float m[E], root[E];
-  uint32_t cw[NW], ro[NB];
+  uint32_t cw[NW], ro[NB * RB];
   float tmin = 3.0e38f, tmax = 0.0f;
   constexpr int NGH = TileIn6<GradT>::NG / 2;
-  uint32_t hl[4], hg[NGH], hr[2], hm[2], hv[2];
+  uint32_t hl[4], hg[NGH], hr[2 * RB], hm[2], hv[2];
 #pragma unroll
   for (int k = 0; k < NW; ++k) {
     const int j = 2 * k;
@@ -382,11 +383,16 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 #pragma unroll
         for (int q = 0; q < NGH; ++q) gmin = min(gmin, hg[q] * 2u - 1u);
       }
+      if (C16) {  // rho == -32768 (formats.py:270-271)
 #pragma unroll
-      for (int q = 0; q < 2; ++q) rmin = __vmins2(rmin, __vmins2(hr[q], hr[q] << 8));
+        for (int q = 0; q < 4; ++q) rmin = __vmins2(rmin, hr[q]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) rmin = __vmins2(rmin, __vmins2(hr[q], hr[q] << 8));
+      }
     }
     const uint32_t w = hl[k & 3];
-    const uint32_t rwd = hr[(j >> 2) & 1], mwd = hm[(j >> 2) & 1], vwd = hv[(j >> 2) & 1];
+    const uint32_t rwd = C16 ? hr[k & 3] : hr[(j >> 2) & 1], mwd = hm[(j >> 2) & 1], vwd = hv[(j >> 2) & 1];
     // reconstruct (formats.py:248-276), see the header comment
     // lp +- R as one IMAD (fast::recon_bits)
     float2 th2;
@@ -394,6 +400,17 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       const int ql = (int)(int8_t)(rwd >> (8 * (j & 3))), qh = (int)(int8_t)(rwd >> (8 * ((j & 3) + 1)));
       th2 = make_float2(reconstruct1(w & 0xFFFFu, ql, __fdiv_rn((float)ql, 127.0f)),
                         reconstruct1(w >> 16, qh, __fdiv_rn((float)qh, 127.0f)));
+    } else if (C16) {
+      // R(rho) = rint_even(RN(rho/32767) * 2^15) computed: the Markstein
+      // quotient with RN(1/32767) is exact for every int16 code
+      // (tests/test_gpu_g32.py::test_int16_every_code), * 2^15 is exact, and
+      // the magic add rounds half-even; |R| <= 2^15 < 2^16 keeps lp + R
+      // inside lp's binade exactly as for int8
+      const float2 q2 = div_y(make_float2((float)(int)(int16_t)(rwd & 0xFFFFu), (float)((int)rwd >> 16)),
+                              dup(32767.0f), dup(0x1.0002p-15f));
+      const float2 t2 = fma2(q2, dup(32768.0f), dup(12582912.0f));
+      const int rl = (int)(__float_as_uint(t2.x) - 0x4B400000u), rh = (int)(__float_as_uint(t2.y) - 0x4B400000u);
+      th2 = make_float2(__uint_as_float(recon_bits(w << 16, rl)), __uint_as_float(recon_bits(w & 0xFFFF0000u, rh)));
     } else {
       const int rl = L.r(rwd, j & 3);
       const int rh = L.r(rwd, (j & 3) + 1);
@@ -413,8 +430,8 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     float2 m2, tn2;
     if (OPT == FO_OPT_ADAMW) {
       const float2 z2 = make_float2(L.v(vwd, j & 3), L.v(vwd, (j & 3) + 1));
-      const float2 r2 = fma2(z2, dup(vsf), Z);
-      const float2 vp2 = fma2(r2, r2, Z);
+      const float2 r2 = fma2(z2, dup(vsf), Z);              // quantize.py:157 (linear: v itself, :185)
+      const float2 vp2 = LINEAR ? r2 : fma2(r2, r2, Z);
       m2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
       const float2 v2 = add2(fma2(dup(h.b2), vp2, Z), fma2(dup(h.omb2), fma2(g2, g2, Z), Z));
       constexpr bool WIDE_ROOT = FO_SQRT_WIDE && (BC & 2) && !SAFE;
@@ -436,11 +453,12 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
           den = add2(rt2, dup(h.eps));
         }
       } else {
-        rt2 = root2<SAFE>(v2);
+        if (!LINEAR) rt2 = root2<SAFE>(v2);
         den = add2(root2<SAFE>(quot_y<SAFE>(v2, h.bc2, h.rbc2)), dup(h.eps));
       }
-      root[j] = rt2.x;
-      root[j + 1] = rt2.y;
+      // the quantity the variance epilogue groups: the root (companded) or v (linear)
+      root[j] = LINEAR ? v2.x : rt2.x;
+      root[j + 1] = LINEAR ? v2.y : rt2.y;
       const float2 u = add2(quot<SAFE>(mh, den), fma2(dup(h.wd), th2, Z));
       tn2 = add2(th2, neg2(fma2(dup(h.lr), u, Z)));
     } else if (OPT == FO_OPT_SGD) {
@@ -462,7 +480,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     m[j] = m2.x;
     m[j + 1] = m2.y;
     // split (formats.py:232-245)
-    uint32_t pr;  // the two correction codes in bytes 0, 1
+    uint32_t pr;  // the two correction codes in bytes 0, 1 (int16: halves 0, 1)
     if (SAFE) {
       uint32_t cl, ch;
       int ql, qh;
@@ -475,6 +493,18 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       cw[k] = *reinterpret_cast<uint32_t*>(&c2);
       const float2 lp2 = make_float2(__uint_as_float(cw[k] << 16), __uint_as_float(cw[k] & 0xFFFF0000u));
       const float2 e2 = add2(tn2, neg2(lp2));  // exact residual
+      if (C16) {
+        // e_n = e * 2^-ell exactly; rho = rint(RN(e_n * 32767)) (formats.py:
+        // 223-225) -- the product is not exact, so RN first, then rint.
+        // K16 = 32767 * 2^-ell * 2^-21 = (32767/16384) * 2^(128 - expf): one
+        // LOP3; RN(e*K16) = RN(e_n*32767) * 2^-21 and 6.0 has ulp 2^-21
+        const float2 k2 = make_float2(__uint_as_float(k16_bits(__float_as_uint(tn2.x))),
+                                      __uint_as_float(k16_bits(__float_as_uint(tn2.y))));
+        // (the product is an FFMA2 with -0 so ptxas cannot contract it into
+        // the add: that would round the exact product once, not twice)
+        const float2 t2 = add2(fma2(e2, k2, Z), dup(6.0f));
+        pr = prmt(__float_as_uint(t2.x), __float_as_uint(t2.y), 0x5410u);
+      } else {
 #if FO_SPLIT_K13
       // K = 127 * 2^-ell with ell = expf(theta) - 135 (the binade-bottom rule
       // is implied by theta's own exponent).  K * 2^-13 = (127/64) *
@@ -496,8 +526,10 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       const float2 q2 = fma2(e2, k2, dup(12582912.0f));
 #endif
       pr = prmt(__float_as_uint(q2.x), __float_as_uint(q2.y), 0x0040u);
+      }
     }
-    if (k & 1) ro[k >> 1] = prmt(ro[k >> 1], pr, 0x5410u);
+    if (C16) ro[k] = pr;
+    else if (k & 1) ro[k >> 1] = prmt(ro[k >> 1], pr, 0x5410u);
     else ro[k >> 1] = pr;
     tmin = fminf(tmin, fminf(fabsf(tn2.x), fabsf(tn2.y)));
     tmax = maxnan3(tmax, fabsf(tn2.x), fabsf(tn2.y));
@@ -520,7 +552,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       bad |= gmin < (0x2E000000u * 2u - 1u);
     }
   }
-  bad |= __vcmplts2(rmin, 0x81008100u) != 0;
+  bad |= __vcmplts2(rmin, C16 ? 0x80018001u : 0x81008100u) != 0;
 
   // ---- epilogue: momentum (quantize.py:109-122), exact ----
   float amax = 0.0f;
@@ -558,12 +590,12 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 #pragma unroll
     for (int o = 1; o < LPG; o <<= 1) rmax = maxnan(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
     bad |= !(rmax <= 65504.0f * RS);
-    new_vsb = (uint32_t)__half_as_ushort(__float2half_ru(RSCALED ? __fmul_rn(rmax, 1.0f / RS) : rmax));
+    new_vsb = (uint32_t)__half_as_ushort(__float2half_ru(QSCALED ? __fmul_rn(rmax, 1.0f / RS) : rmax));
     const float s = half_bits_to_float(new_vsb);
     // RSCALED: RN(root'/(s*2^30)) with y = RN(1/s)*2^-30 is the same
     // Markstein quotient as RN(root/s) with every intermediate scaled exactly
-    const float den = RSCALED ? __fmul_rn((s == 0.0f) ? 1.0f : s, RS) : ((s == 0.0f) ? 1.0f : s);
-    const float y = RSCALED ? __fmul_rn(rcp_rn_normal((s == 0.0f) ? 1.0f : s), 1.0f / RS) : rcp_rn_normal(den);
+    const float den = QSCALED ? __fmul_rn((s == 0.0f) ? 1.0f : s, RS) : ((s == 0.0f) ? 1.0f : s);
+    const float y = QSCALED ? __fmul_rn(rcp_rn_normal((s == 0.0f) ? 1.0f : s), 1.0f / RS) : rcp_rn_normal(den);
 #pragma unroll
     for (int j = 0; j < E; j += 2) {
       const float2 vn = quot_y<SAFE>(make_float2(root[j], root[j + 1]), den, y);  // RN(r/s)
@@ -586,7 +618,13 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 #pragma unroll
     for (int c = 0; c < NW / 4; ++c)
       stcs4(T.lp + e0 + 8 * c, make_uint4(cw[4 * c], cw[4 * c + 1], cw[4 * c + 2], cw[4 * c + 3]));
-    store_bytes<NB>(T.rho + e0, ro);
+    if (C16) {
+      int16_t* r16 = reinterpret_cast<int16_t*>(T.rho) + e0;
+      stcs4(r16, make_uint4(ro[0], ro[1], ro[2], ro[3]));
+      stcs4(r16 + 8, make_uint4(ro[4], ro[5], ro[6], ro[7]));
+    } else {
+      store_bytes<NB>(T.rho + e0, ro);
+    }
     store_bytes<NB>(T.mq + e0, mo);
     if (ADAM) store_bytes<NB>(T.vq + e0, vo);
   } else {
@@ -595,7 +633,8 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       const int64_t i = e0 + j;
       if (i < n) {
         T.lp[i] = (uint16_t)(cw[j >> 1] >> (16 * (j & 1)));
-        T.rho[i] = (int8_t)(ro[j >> 2] >> (8 * (j & 3)));
+        if (C16) reinterpret_cast<int16_t*>(T.rho)[i] = (int16_t)(ro[j >> 1] >> (16 * (j & 1)));
+        else T.rho[i] = (int8_t)(ro[j >> 2] >> (8 * (j & 3)));
         T.mq[i] = (int8_t)(mo[j >> 2] >> (8 * (j & 3)));
         if (ADAM) T.vq[i] = (uint8_t)(vo[j >> 2] >> (8 * (j & 3)));
       }
@@ -609,10 +648,10 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 }
 
 // A full tile straight from global memory with 128-bit loads.
-template <int OPT, typename GradT>
-__device__ __forceinline__ void load6_global_full(const TArg& T, int64_t base, int lane, TileIn6<GradT>& in) {
+template <int OPT, typename GradT, int NCORR = 127>
+__device__ __forceinline__ void load6_global_full(const TArg& T, int64_t base, int lane, TileIn6<GradT, NCORR>& in) {
   constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
-  constexpr int E = FEPL, NG = TileIn6<GradT>::NG;
+  constexpr int E = FEPL, NG = TileIn6<GradT, NCORR>::NG;
   const int64_t e0 = base + (int64_t)lane * E;
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
@@ -624,7 +663,12 @@ __device__ __forceinline__ void load6_global_full(const TArg& T, int64_t base, i
     const uint4 a = ldcs4(reinterpret_cast<const GradT*>(T.g) + e0 + (16 / sizeof(GradT)) * c);
     in.gw[4 * c] = a.x; in.gw[4 * c + 1] = a.y; in.gw[4 * c + 2] = a.z; in.gw[4 * c + 3] = a.w;
   }
-  load_bytes<4>(T.rho + e0, in.rw);
+  if (NCORR == 127) {
+    load_bytes<4>(T.rho + e0, in.rw);
+  } else {
+    load_bytes<4>(reinterpret_cast<const int16_t*>(T.rho) + e0, in.rw);
+    load_bytes<4>(reinterpret_cast<const int16_t*>(T.rho) + e0 + 8, in.rw + 4);
+  }
   load_bytes<4>(T.mq + e0, in.mw);
   if (ADAM) load_bytes<4>(T.vq + e0, in.vw);
   in.msb = T.ms[e0 >> 5];
@@ -633,15 +677,22 @@ __device__ __forceinline__ void load6_global_full(const TArg& T, int64_t base, i
 
 // One flagged slice in the fix-up launch: the SAFE tile (exact everywhere the
 // fast one needed guards), or the straight restatement for error cases.
-template <int OPT, typename GradT, int BC>
+template <int OPT, typename GradT, int BC, int NCORR = 127, bool LINEAR = false>
 __device__ __forceinline__ void safe_tile(const TArg& T, const fo_hparams& h, int64_t base, int lane, float negzero,
                                           uint32_t* err_out) {
-  const bool full = (T.n - base) >= FTILE;
-  TileIn6<GradT> in;
-  if (full) load6_global_full<OPT, GradT>(T, base, lane, in);
-  else load6_global<OPT, GradT>(T, base, lane, in);
-  const RegSrc<GradT> src{in, in.msb, in.vsb};
-  uint32_t err = 0;
-  const NoLut L;
-  compute_tile6<OPT, GradT, BC, RegSrc<GradT>, NoLut, true>(T, h, base, lane, err, L, negzero, err_out, 0, full, src);
+  if constexpr (NCORR != 127 || LINEAR) {
+    // the optional layouts' flagged slices: the straight restatement
+    (void)negzero;
+    process_tile_exact<OPT, GradT, FEPL, NCORR, LINEAR>(T, h, base, lane, err_out);
+    return;
+  } else {
+    const bool full = (T.n - base) >= FTILE;
+    TileIn6<GradT> in;
+    if (full) load6_global_full<OPT, GradT>(T, base, lane, in);
+    else load6_global<OPT, GradT>(T, base, lane, in);
+    const RegSrc<GradT> src{in, in.msb, in.vsb};
+    uint32_t err = 0;
+    const NoLut L;
+    compute_tile6<OPT, GradT, BC, RegSrc<GradT>, NoLut, true>(T, h, base, lane, err, L, negzero, err_out, 0, full, src);
+  }
 }

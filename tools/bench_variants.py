@@ -61,7 +61,10 @@ def run(config: str, opt: str, variant: str, steps: int, warmup: int) -> dict:
     n = fl.numel
     bpp = bytes_per_param(opt, rho_bits)
     peak, _ = bench.peaks()
-    kernel = "step_ws_kernel" if variant == "default" else \
+    # int16 corrections and linear variance take the fused kernel since round 2
+    # (FO_FAST_LAYOUTS=0 keeps them on the exact kernels); misaligned views never do
+    fused = variant == "default" or (variant in ("int16", "linear") and os.environ.get("FO_FAST_LAYOUTS") != "0")
+    kernel = "step_ws_kernel" if fused else \
         ("step_generic_kernel" if os.environ.get("FO_GENERIC") == "pergroup" else "step_g32_kernel")
     return {"config": config, "optimizer": opt, "variant": variant, "kernel": kernel, "params": n,
             "ms_per_step": ms, "gparams_per_s": n / (ms * 1e-3) / 1e9, "bytes_per_param": bpp,

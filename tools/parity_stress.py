@@ -4,7 +4,11 @@ oracle on random optimizers, sizes, states, gradient magnitude ranges
 and step counters, for a wall-clock budget.  Prints one summary JSON line;
 mismatching cases are written to gpurun_out/stress_fail_*.json.
 
-    python tools/parity_stress.py [--seconds 240] [--seed 1]
+    python tools/parity_stress.py [--seconds 240] [--seed 1] [--layouts]
+
+--layouts also draws the optional layouts (int16 corrections, linear
+variance) and training-like weights, which keep most slices on the fused
+tile of those layouts.
 """
 
 from __future__ import annotations
@@ -31,8 +35,11 @@ def pick_beta(rng):
     return float(rng.choice([0.0, 2.0 ** -29, 0.3, 0.9, 0.95, 0.99, 0.999, 1 - 2.0 ** -19]))
 
 
-def random_case(rng):
+def random_case(rng, layouts=False):
     opt = str(rng.choice(["adamw", "sgd", "lion"]))
+    rho_bits = int(rng.choice([8, 16])) if layouts else 8
+    scheme = str(rng.choice(["companded", "linear"])) if (layouts and opt == "adamw") else "companded"
+    training_like = bool(layouts and rng.random() < 0.5)
     n = int(rng.choice([int(rng.integers(1, 5000)), int(rng.integers(5000, 300000)), int(rng.integers(300000, 2000000))]))
     lr = float(10 ** rng.uniform(-8, 0.5))
     wd = float(rng.choice([0.0, 1e-4, 0.01, 0.1, 1.0]))
@@ -47,7 +54,8 @@ def random_case(rng):
     lo, hi = sorted(rng.uniform(-149, 8, 2))
     inject = str(rng.choice(["none"] * 9 + ["nan", "inf", "huge", "rho"])) if rng.random() < 0.3 else "none"
     return dict(opt=opt, n=n, hp=hp, t=t, glo=float(lo), ghi=float(hi), zero_state=bool(rng.random() < 0.2),
-                grad_f32=bool(rng.random() < 0.2), inject=inject, seed=int(rng.integers(0, 2 ** 31)))
+                grad_f32=bool(rng.random() < 0.2), inject=inject, seed=int(rng.integers(0, 2 ** 31)),
+                rho_bits=rho_bits, scheme=scheme, training_like=training_like)
 
 
 def run_case(c, dev):
@@ -55,7 +63,11 @@ def run_case(c, dev):
 
     rng = np.random.default_rng(c["seed"])
     n, opt = c["n"], c["opt"]
-    st = H.random_state(rng, n, opt)
+    rho_bits, scheme = c.get("rho_bits", 8), c.get("scheme", "companded")
+    lp = H.bf16_codes((rng.standard_normal(n) * 0.02).astype(np.float32)) if c.get("training_like") else None
+    st = H.random_state(rng, n, opt, lp=lp)
+    if rho_bits == 16:
+        st["weights.rho"] = rng.integers(-32767, 32768, n).astype(np.int16)
     if c["zero_state"]:
         for k in st:
             if k not in ("weights.lp", "weights.rho"):
@@ -73,10 +85,10 @@ def run_case(c, dev):
     elif c.get("inject") == "huge":
         g[k] = np.float32(3e38)
     elif c.get("inject") == "rho":
-        st["weights.rho"][k] = -128
-    ost = oracle_state(st, c["t"])
+        st["weights.rho"][k] = -128 if rho_bits == 8 else -32768
+    ost = oracle_state(st, c["t"], 32, scheme)
     oerr = O.step_inplace(opt, ost, g, nthreads=8, **c["hp"])
-    fs = to_device(st, c["t"], dev)
+    fs = to_device(st, c["t"], dev, 32, scheme)
     gd = torch.from_numpy(g).to(dev)
     if not c["grad_f32"]:
         gd = gd.bfloat16()
@@ -97,6 +109,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=240)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--layouts", action="store_true")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     rng = np.random.default_rng(args.seed)
@@ -104,7 +117,7 @@ def main():
     counts, elems, fails = {}, 0, 0
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     while time.time() < t_end:
-        c = random_case(rng)
+        c = random_case(rng, args.layouts)
         r = run_case(c, dev)
         key = r if isinstance(r, str) else r[0]
         counts[key] = counts.get(key, 0) + 1
