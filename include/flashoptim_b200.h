@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FO_ABI_VERSION 1
+#define FO_ABI_VERSION 2
 
 /* Return codes (>0 values are cudaError_t). */
 #define FO_OK 0
@@ -154,6 +154,49 @@ int fo_fixup_stats(void *stream, uint64_t *flagged, uint64_t *slices, int reset)
  * elements, so that a CUDA-graph capture of fo_step_mt on that stream
  * allocates nothing.  Optional. */
 int fo_reserve(void *stream, int64_t max_elems);
+/* Elements per CTA tile of the fused kernel: every tensor of a launch is
+ * padded to a multiple of it in the fix-up bitmap, so fo_reserve(stream,
+ * sum of round_up(n_i, fo_fused_tile_elems())) covers any list. */
+int64_t fo_fused_tile_elems(void);
+
+/* Device-resident step scalars for CUDA-graph capture (the role of torch's
+ * `capturable=True`): a captured fo_step_mt_dev reads, every time the graph
+ * runs, the step counter t from device memory and takes (bc1, RN(1/bc1),
+ * bc2, RN(1/bc2)) from a table built by fo_bias_table (entry min(t,
+ * bc_len-1)), and the learning rate from `lr` when it is not NULL.  The
+ * caller advances *step before each step (optim.py:211: t = state.t + 1),
+ * e.g. with a captured device increment. */
+typedef struct fo_dev_scalars {
+  const int32_t *step;   /* device int32: t of the step being taken          */
+  const float *lr;       /* device f32 learning rate, or NULL (hparams->lr)  */
+  const float *bc_table; /* device f32[4 * bc_len] from fo_bias_table        */
+  int32_t bc_len;        /* 0 for SGD / Lion (no bias correction)            */
+  int32_t reserved;
+  /* The caller's fix-up bitmap (zeroed once; every launch leaves it zero):
+   * at least fo_fix_words(tensors) words.  The library allocates nothing. */
+  uint32_t *fix_bits;
+  int64_t fix_words;
+  unsigned long long *fix_count; /* device counter of re-run slices, or NULL */
+} fo_dev_scalars;
+
+/* Words of fix-up bitmap a fused launch over `tensors` needs (a power of two). */
+int64_t fo_fix_words(const fo_tensor *tensors, int32_t n_tensors);
+
+/* fo_step_mt with one hyper-parameter set whose t-dependent fields come from
+ * `dev` (hparams->bc1 ... are ignored).  The default layout only (int8
+ * corrections, companded variance, group size 32, 16-byte aligned views,
+ * hyper-parameters inside the fused tile's ranges): anything else returns
+ * FO_EUNSUPPORTED.  Allocates nothing once fo_reserve has sized the stream's
+ * fix-up bitmap, so it can be captured into a CUDA graph. */
+int fo_step_mt_dev(int optimizer, const fo_tensor *tensors, int32_t n_tensors, const fo_hparams *hparams,
+                   const fo_dev_scalars *dev, int grad_dtype, uint32_t *d_err, void *stream);
+
+/* Host table for fo_dev_scalars: out[4t .. 4t+3] = (bc1, RN(1/bc1), bc2,
+ * RN(1/bc2)) of fo_make_hparams at step t, for t = 0 .. *len-1, where *len-1
+ * is the first t >= 1 at which both corrections are 1.0f (every later t has
+ * the same entry; optim.py:212-213).  out may be NULL to query *len.
+ * FO_ETOOMANY if that needs more than max_len entries. */
+int fo_bias_table(double beta1, double beta2, int32_t max_len, float *out, int32_t *len);
 
 /* Single-tensor steps, in place (optim.py:208, :187, :238). */
 int fo_adamw_step(uint16_t *lp, int8_t *rho, int8_t *m_codes, uint16_t *m_scales, uint8_t *v_codes,

@@ -38,6 +38,13 @@ class fo_hparams(ctypes.Structure):
                 ("lr", "wd", "eps", "b1", "omb1", "b2", "omb2", "mu", "bc1", "bc2", "rbc1", "rbc2")]
 
 
+class fo_dev_scalars(ctypes.Structure):
+    """include/flashoptim_b200.h: device-resident step counter, lr and bias table."""
+    _fields_ = [("step", ctypes.c_void_p), ("lr", ctypes.c_void_p), ("bc_table", ctypes.c_void_p),
+                ("bc_len", ctypes.c_int32), ("reserved", ctypes.c_int32), ("fix_bits", ctypes.c_void_p),
+                ("fix_words", ctypes.c_int64), ("fix_count", ctypes.c_void_p)]
+
+
 class fo_tensor(ctypes.Structure):
     _fields_ = [
         ("lp", ctypes.c_void_p),
@@ -80,6 +87,11 @@ SIGNATURES = {
     "fo_fixup_stats": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64),
                                       ctypes.c_int]),
     "fo_reserve": (ctypes.c_int, [_P, _I64]),
+    "fo_fused_tile_elems": (_I64, []),
+    "fo_fix_words": (_I64, [ctypes.POINTER(fo_tensor), _I32]),
+    "fo_step_mt_dev": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(fo_tensor), _I32, ctypes.POINTER(fo_hparams),
+                                      ctypes.POINTER(fo_dev_scalars), ctypes.c_int, _P, _P]),
+    "fo_bias_table": (ctypes.c_int, [_D, _D, _I32, _P, ctypes.POINTER(_I32)]),
 }
 
 _lib = None
@@ -106,7 +118,7 @@ def lib() -> ctypes.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.fo_abi_version() != 1:
+        if L.fo_abi_version() != 2:
             raise RuntimeError("libflashoptim_b200 ABI version mismatch")
         _lib = L
     return _lib

@@ -99,6 +99,67 @@ int fo_step_mt(int optimizer, const fo_tensor* tensors, int32_t n_tensors, const
                      variance_scheme, d_err, as_stream(stream));
 }
 
+int fo_step_mt_dev(int optimizer, const fo_tensor* tensors, int32_t n_tensors, const fo_hparams* hparams,
+                   const fo_dev_scalars* dev, int grad_dtype, uint32_t* d_err, void* stream) {
+  if (!dev || !dev->step || dev->bc_len < 0 || (dev->bc_len > 0 && !dev->bc_table)) return FO_EINVAL;
+  if (optimizer == FO_OPT_ADAMW && dev->bc_len < 2) return FO_EINVAL;
+  for (int32_t i = 0; i < n_tensors; ++i)
+    if (tensors && tensors[i].hp_index != 0) return FO_EINVAL;
+  if (check_opt(optimizer) || n_tensors < 0 || (n_tensors && !tensors) || !hparams) return FO_EINVAL;
+  if (grad_dtype != FO_GRAD_BF16 && grad_dtype != FO_GRAD_F32) return FO_EINVAL;
+  for (int32_t i = 0; i < n_tensors; ++i) {
+    const fo_tensor& t = tensors[i];
+    if (t.n < 0) return FO_EINVAL;
+    if (t.n == 0) continue;
+    if (!t.lp || !t.rho || !t.m_codes || !t.m_scales || !t.grad) return FO_EINVAL;
+    if (optimizer == FO_OPT_ADAMW && (!t.v_codes || !t.v_scales)) return FO_EINVAL;
+  }
+  // the fused tile's hyper-parameter ranges are checked on the first
+  // (smallest) bias corrections of the run, t = 1
+  // (bc at t = 1 is f32(1 - beta) = omb, fo_make_hparams; nothing is read
+  // back from the device, so the call stays capturable)
+  fo_hparams h = *hparams;
+  if (optimizer == FO_OPT_ADAMW) {
+    volatile float one = 1.0f;
+    h.bc1 = h.omb1;
+    h.bc2 = h.omb2;
+    h.rbc1 = one / h.bc1;
+    h.rbc2 = one / h.bc2;
+  }
+  if (!dev->fix_bits || dev->fix_words < fo::fix_words_for(tensors, n_tensors)) return FO_EINVAL;
+  const fo::DevScalars ds{dev->step, dev->lr, dev->bc_table, dev->bc_len, dev->fix_bits, dev->fix_words,
+                          dev->fix_count};
+  return fo::step_mt(optimizer, tensors, n_tensors, &h, 1, grad_dtype, 8, 32, FO_VAR_COMPANDED, d_err,
+                     as_stream(stream), &ds);
+}
+
+int fo_bias_table(double beta1, double beta2, int32_t max_len, float* out, int32_t* len) {
+  if (!len || max_len < 2 || !(beta1 >= 0.0 && beta1 < 1.0) || !(beta2 >= 0.0 && beta2 < 1.0)) return FO_EINVAL;
+  int32_t n = 0;
+  for (int64_t t = 0;; ++t) {
+    if (t >= max_len) return FO_ETOOMANY;
+    fo_hparams h;
+    fo_make_hparams(FO_OPT_ADAMW, 1.0, beta1, beta2, 1.0, 0.0, 0.0, t, &h);
+    if (out) {
+      out[4 * t] = h.bc1;
+      out[4 * t + 1] = h.rbc1;
+      out[4 * t + 2] = h.bc2;
+      out[4 * t + 3] = h.rbc2;
+    }
+    n = (int32_t)t + 1;
+    if (t >= 1 && h.bc1 == 1.0f && h.bc2 == 1.0f) break;
+  }
+  *len = n;
+  return 0;
+}
+
+int64_t fo_fused_tile_elems(void) { return fo::fused_tile_elems(); }
+
+int64_t fo_fix_words(const fo_tensor* tensors, int32_t n_tensors) {
+  if (n_tensors < 0 || (n_tensors && !tensors)) return FO_EINVAL;
+  return fo::fix_words_for(tensors, n_tensors);
+}
+
 int fo_step_host(int optimizer, const fo_tensor* tensors, int32_t n_tensors, const fo_hparams* hparams,
                  int32_t n_hparams, int grad_dtype, int rho_bits, int32_t group_size, int variance_scheme,
                  int64_t chunk_elems, uint32_t* h_err) {

@@ -14,8 +14,21 @@
 
 namespace fo {
 
+// Device-resident step scalars (fo_step_mt_dev): NULL `step` = host scalars.
+struct DevScalars {
+  const int32_t* step;
+  const float* lr;
+  const float* bc;  // 4 floats per t
+  int32_t bc_len;
+  uint32_t* fix_bits;  // caller-owned fix-up bitmap (no allocation on the launch path)
+  int64_t fix_words;
+  unsigned long long* fix_count;
+};
+int64_t fix_words_for(const fo_tensor* ts, int32_t nt);  // fo_step_adamw.cu
+
 int step_mt(int opt, const fo_tensor* ts, int32_t nt, const fo_hparams* hps, int32_t nhp, int grad_dtype,
-            int rho_bits, int32_t G, int var_scheme, uint32_t* d_err, cudaStream_t s);
+            int rho_bits, int32_t G, int var_scheme, uint32_t* d_err, cudaStream_t s,
+            const DevScalars* dev = nullptr);
 int split(const float* theta, int64_t n, uint16_t* lp, void* rho, int rho_bits, uint32_t* d_err, cudaStream_t s);
 int reconstruct(const uint16_t* lp, const void* rho, int rho_bits, int64_t n, float* out, uint32_t* d_err,
                 cudaStream_t s);
@@ -37,6 +50,7 @@ FixBuf fix_buffer(cudaStream_t s, size_t words);
 void fix_account(cudaStream_t s, uint64_t slices);  // host-side count of fast-tile slices launched
 int fix_stats(cudaStream_t s, uint64_t* flagged, uint64_t* slices, int reset);
 int fix_reserve(cudaStream_t s, int64_t elems);
+int64_t fused_tile_elems();  // fo_step_adamw.cu (WS_CT)
 // Persistent-grid size of `kernel` on the current device (cached per kernel and device).
 int grid_cap_for(const void* kernel, int threads, int smem);
 int selftest(int mode, uint64_t begin, uint64_t count, unsigned long long* d_out, cudaStream_t s);

@@ -4,10 +4,10 @@
 namespace fo {
 
 int step_lion(const fo_tensor* ts, int32_t nt, const fo_hparams* hps, int32_t nhp, int grad_dtype, int rho_bits,
-             int32_t G, int var_scheme, uint32_t* d_err, cudaStream_t s) {
+             int32_t G, int var_scheme, uint32_t* d_err, cudaStream_t s, const DevScalars* dev) {
   return grad_dtype == FO_GRAD_BF16
-             ? step_mt_typed<FO_OPT_LION, __nv_bfloat16>(ts, nt, hps, nhp, rho_bits, G, var_scheme, d_err, s)
-             : step_mt_typed<FO_OPT_LION, float>(ts, nt, hps, nhp, rho_bits, G, var_scheme, d_err, s);
+             ? step_mt_typed<FO_OPT_LION, __nv_bfloat16>(ts, nt, hps, nhp, rho_bits, G, var_scheme, d_err, s, dev)
+             : step_mt_typed<FO_OPT_LION, float>(ts, nt, hps, nhp, rho_bits, G, var_scheme, d_err, s, dev);
 }
 
 }  // namespace fo

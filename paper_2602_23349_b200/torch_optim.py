@@ -31,6 +31,16 @@ kernels in a device word; `check_errors` chooses when the host reads it:
 the next step() once it has arrived, never blocking), True / "sync" (read
 after every step, which waits for the step) or False (only when
 raise_errors() is called).  See _errors.ErrorPolicy.
+
+capturable=True (torch.optim's meaning): optimizer.step() can be captured
+into a CUDA graph and replayed.  The step counter of each param group lives
+in a device int32 tensor (state["step"], shared by the group's parameters)
+that step() advances with a device increment, the bias corrections come from
+a device table (fo_bias_table) indexed by it, and a CUDA-tensor group "lr"
+is read from device memory, so a replay computes the same bytes as an eager
+step (fo_step_mt_dev).  The default layout only (int8 corrections, group
+size 32); errors are read with raise_errors() (nothing is read back while a
+graph is being captured).
 """
 
 from __future__ import annotations
@@ -56,18 +66,26 @@ class FlashOptimizer(torch.optim.Optimizer):
 
     OPT = ""
 
-    def __init__(self, params, defaults: dict, *, check_errors: bool | str = "deferred", group_size: int = 32):
+    def __init__(self, params, defaults: dict, *, check_errors: bool | str = "deferred", group_size: int = 32,
+                 capturable: bool = False):
         if check_errors not in (True, False, None, "sync", "deferred", "off"):
             raise ValueError(f"check_errors must be True, False, 'sync', 'deferred' or 'off', got {check_errors!r}")
+        if capturable and group_size != 32:
+            raise ValueError("capturable=True needs group_size 32 (the fused kernel's layout)")
         self.check_errors = check_errors
+        self.capturable = bool(capturable)
         self.spec = GroupSpec(group_size)
         super().__init__(params, defaults)
+        self._cap: dict = {}
         for group in self.param_groups:
             self.hp(group)  # validate with the reference's rules
             for p in group["params"]:
                 self._init_state(p)
         self._errors: ErrorPolicy | None = None
         self._plans: dict = {}
+        if self.capturable:
+            for gi in range(len(self.param_groups)):
+                self._cap_group(gi)
 
     # -- state -----------------------------------------------------------------
     def _init_state(self, p: torch.Tensor) -> None:
@@ -106,6 +124,87 @@ class FlashOptimizer(torch.optim.Optimizer):
 
     def hp(self, group: dict):
         raise NotImplementedError
+
+    # -- capturable step ----------------------------------------------------------
+    def _cap_group(self, gi: int) -> dict:
+        """Device step counter, bias table and fix-up bitmap of param group gi
+        (built before any capture: nothing here may run inside one)."""
+        c = self._cap.get(gi)
+        if c is not None:
+            return c
+        group = self.param_groups[gi]
+        ps = list(group["params"])
+        if not ps:
+            return {}
+        dev = ps[0].device
+        steps = {int(self.state[p]["step"]) for p in ps}
+        if len(steps) != 1:
+            raise ValueError("capturable=True needs one step counter per param group")
+        step = torch.full((), steps.pop(), dtype=torch.int32, device=dev)
+        for p in ps:
+            if self.state[p]["weights.rho"].dtype != torch.int8:
+                raise ValueError("capturable=True takes int8 corrections only")
+            self.state[p]["step"] = step
+        table, n = None, 0
+        if self.OPT == "adamw":
+            b1, b2 = (float(x) for x in group["betas"])
+            ln = ctypes.c_int32(0)
+            _lib.check(_lib.lib().fo_bias_table(b1, b2, 1 << 26, None, ctypes.byref(ln)), "fo_bias_table")
+            n = int(ln.value)
+            host = (ctypes.c_float * (4 * n))()
+            _lib.check(_lib.lib().fo_bias_table(b1, b2, n, ctypes.cast(host, ctypes.c_void_p), ctypes.byref(ln)),
+                       "fo_bias_table")
+            table = torch.frombuffer(bytearray(host), dtype=torch.float32).to(dev)
+        tens = (_lib.fo_tensor * len(ps))()
+        for i, p in enumerate(ps):
+            tens[i].n = p.numel()
+        words = int(_lib.lib().fo_fix_words(tens, len(ps)))
+        c = dict(step=step, table=table, bc_len=n, fix=torch.zeros(words, dtype=torch.int32, device=dev),
+                 count=torch.zeros(1, dtype=torch.int64, device=dev), betas=group.get("betas"), key=None,
+                 tensors=None, hp=None, hp_key=None)
+        self._cap[gi] = c
+        return c
+
+    def _step_capturable(self, gi: int, group: dict, ps: list) -> None:
+        c = self._cap_group(gi)
+        if group.get("betas") != c["betas"]:
+            raise ValueError("capturable=True: betas changed after the bias table was built")
+        key = (tuple(id(p) for p in ps), tuple(p.data_ptr() for p in ps))
+        if c["key"] != key:
+            if len(ps) != len(group["params"]):
+                raise ValueError("capturable=True: every parameter of a group needs a gradient")
+            adam = self.OPT == "adamw"
+            tens = (_lib.fo_tensor * len(ps))()
+            for i, p in enumerate(ps):
+                st, e = self.state[p], tens[i]
+                e.lp, e.rho = p.data.data_ptr(), st["weights.rho"].data_ptr()
+                e.m_codes, e.m_scales = st["momentum.codes"].data_ptr(), st["momentum.scales"].data_ptr()
+                e.v_codes = st["variance.codes"].data_ptr() if adam else None
+                e.v_scales = st["variance.scales"].data_ptr() if adam else None
+                e.n = p.numel()
+            c["key"], c["tensors"] = key, tens
+        tens = c["tensors"]
+        for i, p in enumerate(ps):
+            g = p.grad
+            if g.dtype != torch.bfloat16 or not g.is_contiguous():
+                raise ValueError("capturable=True needs contiguous bf16 gradients")
+            tens[i].grad = g.data_ptr()
+        lr = group["lr"]
+        lr_dev = isinstance(lr, torch.Tensor)
+        if lr_dev and (lr.dtype != torch.float32 or lr.device != ps[0].device or lr.numel() != 1):
+            raise ValueError("a tensor lr must be a one-element float32 tensor on the parameters' device")
+        hp_key = tuple((k, v) for k, v in group.items() if k not in ("params", "lr")) + \
+            (("lr", None if lr_dev else lr),)
+        if c["hp_key"] != hp_key:
+            g2 = dict(group, lr=1.0 if lr_dev else lr)  # a device lr is never read from here
+            c["hp"], c["hp_key"] = (_lib.fo_hparams * 1)(self.hp(g2).scalars(1)), hp_key
+        c["step"].add_(1)  # optim.py:211, t = state.t + 1, on the device
+        ds = _lib.fo_dev_scalars(c["step"].data_ptr(), lr.data_ptr() if lr_dev else None,
+                                 c["table"].data_ptr() if c["table"] is not None else None, c["bc_len"], 0,
+                                 c["fix"].data_ptr(), c["fix"].numel(), c["count"].data_ptr())
+        _lib.check(_lib.lib().fo_step_mt_dev(
+            _lib.OPT_TAGS[self.OPT], tens, len(ps), c["hp"], ctypes.byref(ds), _lib.FO_GRAD_BF16,
+            self._errors.ptr, stream_handle(ps[0].device)), "fo_step_mt_dev")
 
     # -- step ------------------------------------------------------------------
     def _rho_bits(self, p: torch.Tensor) -> int:
@@ -215,9 +314,11 @@ class FlashOptimizer(torch.optim.Optimizer):
             dev = ps[0].device
             if self._errors is None or self._errors.errors.word.device != dev:
                 self._errors = ErrorPolicy(self.check_errors, dev)
-            if not self._launch_cached(gi, group, ps):
+            if self.capturable:
+                self._step_capturable(gi, group, ps)
+            elif not self._launch_cached(gi, group, ps):
                 self._launch(ps, [p.grad.reshape(-1) for p in ps], group)
-        if dev is not None:
+        if dev is not None and not (self.capturable and torch.cuda.is_current_stream_capturing()):
             self._errors.after_step(self.OPT)
         return loss
 
@@ -291,6 +392,10 @@ class FlashOptimizer(torch.optim.Optimizer):
         for g in self.param_groups:
             for p in g["params"]:
                 self._init_state(p)
+        if self.capturable:  # one device counter per group again, from the loaded values
+            self._cap = {}
+            for gi in range(len(self.param_groups)):
+                self._cap_group(gi)
 
 
 class FlashAdamW(FlashOptimizer):

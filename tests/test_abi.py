@@ -42,7 +42,7 @@ def test_abi_version_and_status_strings():
     from paper_2602_23349_b200 import _lib
 
     L = _lib.lib()
-    assert L.fo_abi_version() == 1
+    assert L.fo_abi_version() == 2
     assert L.fo_status_string(0) == b"ok"
     assert L.fo_status_string(-1) == b"invalid argument"
 
@@ -133,3 +133,47 @@ def test_hyperparameter_validation_mirrors_reference():
         FO.AdamHyperParams(lr=0.1, weight_decay=-1.0)
     assert FO.AdamHyperParams(lr=1.0) == FO.AdamHyperParams(lr=1.0, beta1=0.9, beta2=0.999, eps=1e-8,
                                                             weight_decay=0.0)
+
+
+@pytest.mark.parametrize("beta1,beta2", [(0.9, 0.95), (0.9, 0.999), (0.5, 0.6), (0.0, 0.9)])
+def test_bias_table_matches_make_hparams(beta1, beta2):
+    """fo_bias_table (the capturable step's device table) holds exactly the
+    bias corrections fo_make_hparams gives the host path at every t, and ends
+    at the first t where both are 1.0f (optim.py:212-213)."""
+    from paper_2602_23349_b200 import _lib
+
+    L = _lib.lib()
+    n = ctypes.c_int32(0)
+    assert L.fo_bias_table(beta1, beta2, 1 << 22, None, ctypes.byref(n)) == 0
+    n = n.value
+    out = (ctypes.c_float * (4 * n))()
+    m = ctypes.c_int32(0)
+    assert L.fo_bias_table(beta1, beta2, n, ctypes.cast(out, ctypes.c_void_p), ctypes.byref(m)) == 0
+    assert m.value == n
+    tab = np.frombuffer(out, dtype=np.float32).reshape(n, 4)
+    for t in list(range(min(n, 400))) + [n - 1]:
+        hp = _lib.make_hparams("adamw", 1e-3, beta1, beta2, 1e-8, 0.0, t=t)
+        assert (tab[t] == np.array([hp.bc1, hp.rbc1, hp.bc2, hp.rbc2], dtype=np.float32)).all(), t
+    assert tab[-1][0] == 1.0 and tab[-1][2] == 1.0
+    assert n == 2 or not (tab[-2][0] == 1.0 and tab[-2][2] == 1.0)
+    small = ctypes.c_int32(0)
+    assert L.fo_bias_table(0.9, 0.9999, 1000, None, ctypes.byref(small)) == -3  # needs ~1.7e5 entries
+
+
+def test_capturable_entry_points_validate_synchronously():
+    from paper_2602_23349_b200 import _lib
+
+    L = _lib.lib()
+    assert L.fo_fused_tile_elems() == 8192
+    ts = (_lib.fo_tensor * 3)()
+    for i, n in enumerate((1, 8192, 8193)):
+        ts[i].n = n
+    # 1 + 1 + 2 CTA tiles of 16 slices = 64 slices -> 2 words
+    assert L.fo_fix_words(ts, 3) == 2
+    hp = _lib.make_hparams("adamw", 1e-3)
+    ds = _lib.fo_dev_scalars()
+    assert L.fo_step_mt_dev(1, None, 0, ctypes.byref(hp), ctypes.byref(ds), 0, None, None) == -1  # no step ptr
+    ds.step = 16
+    assert L.fo_step_mt_dev(1, None, 0, ctypes.byref(hp), ctypes.byref(ds), 0, None, None) == -1  # adamw: no table
+    ds.bc_table, ds.bc_len = 16, 40
+    assert L.fo_step_mt_dev(1, None, 0, ctypes.byref(hp), ctypes.byref(ds), 0, None, None) == -1  # no bitmap
