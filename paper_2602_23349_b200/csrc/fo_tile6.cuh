@@ -101,7 +101,14 @@ struct NoLut {
 // offset -> byte 0, 0x02 -> byte 2): no address arithmetic at all, and the
 // lanes of a warp hit distinct banks except l and l+21 (at most 2-way
 // conflicts, against ~3.5-way for random indices into a compact table).
-constexpr int WIDE_COPIES = 21;
+// FO_R_LUT=0: R(rho) is computed (see compute_tile6) and the wide LUT holds
+// only the two moment tables, 32 copies each: lane l reads word l of its
+// table's half row, so every lookup is conflict-free.
+#ifndef FO_R_LUT
+#define FO_R_LUT 1
+#endif
+constexpr int WIDE_COPIES = FO_R_LUT ? 21 : 32;
+constexpr int WIDE_TABLES = FO_R_LUT ? 3 : 2;
 constexpr uint32_t WIDE_LUT_ADDR = 0x20000u;
 constexpr uint32_t WIDE_LUT_BYTES = 256u * 256u;
 struct WideLut {
@@ -129,12 +136,13 @@ __device__ __forceinline__ WideLut init_wide_lut(uint8_t* dsm, Luts6& Ls) {
   uint8_t* base = dsm + (WIDE_LUT_ADDR - (uint32_t)__cvta_generic_to_shared(dsm));
   init_luts6(Ls);
   __syncthreads();
-  for (int i = threadIdx.x; i < 256 * 3 * WIDE_COPIES; i += blockDim.x) {
-    const int b = i / (3 * WIDE_COPIES), w = i % (3 * WIDE_COPIES), t = w / WIDE_COPIES;
+  for (int i = threadIdx.x; i < 256 * WIDE_TABLES * WIDE_COPIES; i += blockDim.x) {
+    const int b = i / (WIDE_TABLES * WIDE_COPIES), w = i % (WIDE_TABLES * WIDE_COPIES), t = w / WIDE_COPIES + (3 - WIDE_TABLES);
     const uint32_t val = t == 0 ? (uint32_t)Ls.r[b] : __float_as_uint(t == 1 ? Ls.m[b] : Ls.v[b]);
     reinterpret_cast<uint32_t*>(base + b * 256)[w] = val;
   }
   const uint32_t c = (threadIdx.x & 31) % WIDE_COPIES;
+  if (WIDE_TABLES == 2) return WideLut{0u, WIDE_LUT_ADDR | (4u * c), WIDE_LUT_ADDR | (4u * (WIDE_COPIES + c))};
   return WideLut{WIDE_LUT_ADDR | (4u * c), WIDE_LUT_ADDR | (4u * (WIDE_COPIES + c)),
                  WIDE_LUT_ADDR | (4u * (2 * WIDE_COPIES + c))};
 }
@@ -409,6 +417,18 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       const float2 q2 = div_y(make_float2((float)(int)(int16_t)(rwd & 0xFFFFu), (float)((int)rwd >> 16)),
                               dup(32767.0f), dup(0x1.0002p-15f));
       const float2 t2 = fma2(q2, dup(32768.0f), dup(12582912.0f));
+      const int rl = (int)(__float_as_uint(t2.x) - 0x4B400000u), rh = (int)(__float_as_uint(t2.y) - 0x4B400000u);
+      th2 = make_float2(__uint_as_float(recon_bits(w << 16, rl)), __uint_as_float(recon_bits(w & 0xFFFF0000u, rh)));
+    } else if (!FO_R_LUT) {
+      // R(rho) = rint(rho * RN(32768/127)) in one FFMA2: rho * 32768/127 is
+      // at least 0.5/127 away from any half-integer and RN(32768/127) moves
+      // rho * it by < 0.002, so this equals rint_even(RN(rho/127) * 2^15)
+      // for every int8 code (tests/test_reconstruct_int.py).  float(rho)
+      // exactly: bytes (rho + 128) | 0x4B000000 = 2^23 + rho + 128.
+      const uint32_t wx = rwd ^ 0x80808080u;
+      const float2 fx = make_float2(__uint_as_float(prmt(wx, 0x4B000000u, 0x7440u + (j & 3))),
+                                    __uint_as_float(prmt(wx, 0x4B000000u, 0x7441u + (j & 3))));
+      const float2 t2 = fma2(add2(fx, dup(-8388736.0f)), dup(32768.0f / 127.0f), dup(12582912.0f));
       const int rl = (int)(__float_as_uint(t2.x) - 0x4B400000u), rh = (int)(__float_as_uint(t2.y) - 0x4B400000u);
       th2 = make_float2(__uint_as_float(recon_bits(w << 16, rl)), __uint_as_float(recon_bits(w & 0xFFFF0000u, rh)));
     } else {
