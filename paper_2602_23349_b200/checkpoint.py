@@ -349,3 +349,5 @@ def load_optimizer(optimizer, directory) -> None:
                 st["variance.codes"] = fs.variance.codes.view(p.shape).clone()
                 st["variance.scales"] = fs.variance.scales.clone()
             st["step"] = fs.t
+    if hasattr(optimizer, "_reset_capturable"):
+        optimizer._reset_capturable()

@@ -47,6 +47,8 @@ class GradientRelease:
     def __init__(self, optimizer, stream: torch.cuda.Stream | None = None, bucket_elems: int = 1 << 25,
                  check_errors: bool | str = "deferred", timing: bool = False):
         self.opt = optimizer
+        if getattr(optimizer, "capturable", False):
+            raise ValueError("gradient release steps from backward hooks; use an optimizer with capturable=False")
         params = [p for g in optimizer.param_groups for p in g["params"]]
         if not params:
             raise ValueError("optimizer has no parameters")

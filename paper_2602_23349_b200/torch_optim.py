@@ -392,7 +392,13 @@ class FlashOptimizer(torch.optim.Optimizer):
         for g in self.param_groups:
             for p in g["params"]:
                 self._init_state(p)
-        if self.capturable:  # one device counter per group again, from the loaded values
+        self._reset_capturable()
+
+    def _reset_capturable(self) -> None:
+        """After the state tensors were replaced (load_state_dict,
+        checkpoint.load_optimizer): one device step counter per group again,
+        from the loaded values, and fresh launch tables."""
+        if self.capturable:
             self._cap = {}
             for gi in range(len(self.param_groups)):
                 self._cap_group(gi)

@@ -152,3 +152,39 @@ def test_capturable_state_dict_round_trip(cuda_dev):
     cap2.step()
     torch.cuda.synchronize()
     assert _same(_state_bytes(cap, pc), _state_bytes(cap2, pc2))
+
+
+def test_capturable_flop_checkpoint_round_trip(cuda_dev, tmp_path):
+    """checkpoint.save_optimizer / load_optimizer into a capturable optimizer:
+    the loaded state gets one device counter per group and fresh launch
+    tables, and steps on bitwise like the original."""
+    import paper_2602_23349_b200.torch_optim as P
+    from paper_2602_23349_b200 import checkpoint
+
+    pc = _params(cuda_dev, 4)
+    cap = P.FlashAdamW(pc, lr=1e-3, betas=(0.9, 0.95), capturable=True)
+    for p in pc:
+        p.grad = (torch.randn_like(p, dtype=torch.float32) * 1e-2).bfloat16()
+    for _ in range(4):
+        cap.step()
+    checkpoint.save_optimizer(cap, str(tmp_path))
+    pc2 = [torch.nn.Parameter(torch.zeros(n, device=cuda_dev)) for n in SIZES]
+    cap2 = P.FlashAdamW(pc2, lr=1e-3, betas=(0.9, 0.95), capturable=True)
+    checkpoint.load_optimizer(cap2, str(tmp_path))
+    assert int(cap2.state[pc2[0]]["step"]) == 4
+    assert cap2.state[pc2[0]]["step"] is cap2.state[pc2[-1]]["step"]
+    for p, q in zip(pc, pc2):
+        q.grad = p.grad.clone()
+    cap.step()
+    cap2.step()
+    torch.cuda.synchronize()
+    assert _same(_state_bytes(cap, pc), _state_bytes(cap2, pc2))
+
+
+def test_release_refuses_capturable(cuda_dev):
+    import paper_2602_23349_b200.torch_optim as P
+    from paper_2602_23349_b200.release import GradientRelease
+
+    opt = P.FlashSGD(_params(cuda_dev, 5), lr=0.1, capturable=True)
+    with pytest.raises(ValueError, match="capturable"):
+        GradientRelease(opt)

@@ -92,3 +92,32 @@ def test_install_routes_reference_api(cuda_dev):
     finally:
         B.uninstall(fo, orig)
     assert O.adamw_step is orig["adamw"]
+
+
+@pytest.mark.parametrize("width_bits", [8, 16])
+@pytest.mark.parametrize("scheme", ["companded", "linear"])
+def test_binding_optional_layouts_trajectory(width_bits, scheme, cuda_dev):
+    """The reference's optional layouts through the binding: INT16_CORRECTION
+    weights (formats.py:94-95) and the linear variance scheme
+    (optim.py:164-175), ten AdamW steps from init, bitwise equal to the
+    reference's NumPy trajectory after every step."""
+    from paper_2602_23349_b200 import flashopt_binding as B
+
+    fo = RB.flashopt()
+    O, F = fo.optim, fo.formats
+    rng = np.random.default_rng(700 + width_bits + (1 if scheme == "linear" else 0))
+    n = 40_003
+    theta0 = H.random_weights(rng, n)
+    width = F.INT16_CORRECTION if width_bits == 16 else F.INT8_CORRECTION
+    a = O.init_flash_state(theta0, "adamw", variance_scheme=scheme)
+    a.weights = F.SplitTensor.from_values(theta0, F.BF16, width)
+    b = O.init_flash_state(theta0, "adamw", variance_scheme=scheme)
+    b.weights = F.SplitTensor.from_values(theta0, F.BF16, width)
+    hp = O.AdamHyperParams(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1)
+    for _ in range(10):
+        g = H.random_grad(rng, n, std=1e-2)
+        a = B.step("adamw", a, g, hp)
+        b = O.adamw_step(b, g, hp)
+        assert a.weights.corrections.dtype == b.weights.corrections.dtype
+        mm = _same(RB.from_ref_state(a), RB.from_ref_state(b))
+        assert all(v == 0 for v in mm.values()), mm
