@@ -1,7 +1,9 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): every kernel family of libflashoptim_b200.so on a few tensors,
 with slices that trip the fast tile's guards (so the fix-up launch runs),
-and the host streaming path with a group size below 32.  Checks results
+int16 corrections and linear variance on the fused kernel, the capturable
+(device-scalar) instances, and the host streaming path with a group size
+below 32.  Checks results
 against the C oracle too, so a sanitizer run is also a parity run.
 
     compute-sanitizer --tool memcheck python tools/sanitize_driver.py
@@ -62,6 +64,37 @@ for opt in ("adamw", "sgd", "lion"):
         if opt == "adamw":
             d.update({"variance.codes": h.v_codes, "variance.scales": h.v_scales})
         check(f"host {opt} G=16", d, ost)
+# linear variance on the fused kernel (int8 and int16 corrections)
+for rho16 in (False, True):
+    n = 12000 + 5
+    st = H.random_state(rng, n, "adamw", rho=rng.integers(-32767, 32768, n).astype(np.int16) if rho16 else None)
+    g = H.random_grad(rng, n)
+    hp = H.random_hparams(rng, "adamw")
+    fs = to_device(st, 5, dev, 32, "linear")
+    FO.adamw_step_(fs, torch.from_numpy(g).to(dev).bfloat16(), FO.AdamHyperParams(**hp))
+    ost = oracle_state(st, 5, 32, "linear")
+    assert O.step_inplace("adamw", ost, g, **hp) == 0
+    check(f"adamw linear rho16={rho16}", from_device(fs), ost)
+# the capturable (device-scalar) kernels against the eager optimizer
+import paper_2602_23349_b200.torch_optim as TO  # noqa: E402
+
+for name in ("FlashAdamW", "FlashSGD", "FlashLion"):
+    gen = torch.Generator().manual_seed(3)
+    ps = [torch.nn.Parameter((torch.randn(n, generator=gen) * 0.02).to(dev)) for n in (5000, 70)]
+    pe = [torch.nn.Parameter(p.detach().clone()) for p in ps]
+    cap = getattr(TO, name)(ps, lr=1e-3, capturable=True)
+    eag = getattr(TO, name)(pe, lr=1e-3)
+    for _ in range(3):
+        gs = [(torch.randn(p.numel(), generator=gen) * 1e-2).bfloat16().to(dev) for p in ps]
+        for p, q, g in zip(ps, pe, gs):
+            p.grad, q.grad = g.clone(), g.clone()
+        cap.step()
+        eag.step()
+    torch.cuda.synchronize()
+    for p, q in zip(ps, pe):
+        if not torch.equal(p.data.view(torch.int16), q.data.view(torch.int16)):
+            bad += 1
+            print("MISMATCH capturable", name)
 torch.cuda.synchronize()
 f, s = _lib.fixup_stats(reset=True)
 print(f"sanitize_driver: {bad} mismatching cases; fix-up slices {f} of {s}")
