@@ -740,7 +740,8 @@ def run_ours(args) -> None:
         from paper_2602_23349_b200.zero import ZeroFlashOptimizer
 
         params = [torch.empty(s, dtype=torch.bfloat16, device=dev) for _, s in shapes]
-        zo = ZeroFlashOptimizer(params, opt, [hp], bucket_elems=args.bucket_elems, check_errors="off")
+        zo = ZeroFlashOptimizer(params, opt, [hp], bucket_elems=args.bucket_elems, check_errors="off",
+                                fused_allgather=args.fused_ag)
         del params
         init_random_state(zo.flat_state, zo.flat_grads, 1234 + rank, lp=zo.flat_params)
         states = zo.states
@@ -887,9 +888,12 @@ def zero1_phases(zo, args, dev, stream, reduce_, n_all) -> dict:
         a.record(stream)
         zo.reduce_scatter_grads()
         b.record(stream)
-        zo.step_shard()
+        zo.step_shard()  # fused_allgather: the step also writes every peer's parameters
         c.record(stream)
-        zo.all_gather_params()
+        if zo.fused_allgather:
+            zo._peer_barrier()
+        else:
+            zo.all_gather_params()
         d.record(stream)
         zo.t += 1
     torch.cuda.synchronize()
@@ -903,10 +907,15 @@ def zero1_phases(zo, args, dev, stream, reduce_, n_all) -> dict:
     W = zo.world
     total = zo.layout.total
     moved = 2 * (W - 1) / W * total * 2  # bytes each rank sends + receives per RS + AG pair (ring model)
-    return {"reduce_scatter_ms": rs, "step_ms": st, "all_gather_ms": ag, "full_step_ms": full,
-            "full_step_gparams_s": n_all / (full * 1e-3) / 1e9, "params_padded": total,
-            "buckets": len(zo.layout.buckets), "busbw_gbs": moved / ((rs + ag) * 1e-3) / 1e9,
-            "note": "ZeroFlashOptimizer phases; NCCL reduce-scatter (AVG) of bf16 grads, all-gather of bf16 params"}
+    coll = "NCCL" if zo.backend == "nccl" else "gloo (host-staged test mode)"
+    out = {"reduce_scatter_ms": rs, "step_ms": st, "all_gather_ms": ag, "full_step_ms": full,
+           "full_step_gparams_s": n_all / (full * 1e-3) / 1e9, "params_padded": total,
+           "buckets": len(zo.layout.buckets), "busbw_gbs": moved / ((rs + ag) * 1e-3) / 1e9,
+           "fused_allgather": zo.fused_allgather,
+           "note": f"ZeroFlashOptimizer phases; {coll} reduce-scatter of bf16 grads, "
+                   + ("fused step storing every peer's bf16 params over CUDA IPC + cross-rank barrier "
+                      "(all_gather_ms = the barrier)" if zo.fused_allgather else f"{coll} all-gather of bf16 params")}
+    return out
 
 
 def main():
@@ -924,6 +933,8 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--parity-windows", type=int, default=64)
     ap.add_argument("--bucket-elems", type=int, default=None, help="N>1: ZeRO bucket size (default: one bucket)")
+    ap.add_argument("--fused-ag", action="store_true",
+                    help="N>1: fused step + all-gather (the step stores into every peer's parameters, CUDA IPC)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per launch (read+write), from profiles/, reported beside the roofline")
     ap.add_argument("--t0", type=int, default=1000,

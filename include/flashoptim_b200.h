@@ -72,6 +72,7 @@ extern "C" {
 #define FO_VAR_LINEAR 1
 
 #define FO_MAX_HPARAMS 16
+#define FO_MAX_PEERS 7 /* peer mirrors per fo_step_mt_peers call (8 GPUs) */
 
 /* Per-step float32 scalars, formed on the host exactly as the reference
  * forms them: Python floats rounded once to f32 (NEP 50), 1-beta and the
@@ -190,6 +191,26 @@ int64_t fo_fix_words(const fo_tensor *tensors, int32_t n_tensors);
  * fix-up bitmap, so it can be captured into a CUDA graph. */
 int fo_step_mt_dev(int optimizer, const fo_tensor *tensors, int32_t n_tensors, const fo_hparams *hparams,
                    const fo_dev_scalars *dev, int grad_dtype, uint32_t *d_err, void *stream);
+
+/* Fused step + all-gather over peer memory (ZeRO-1, zero.py): fo_step_mt
+ * whose kernels also store every updated weights.lp value at
+ * (char *)lp + peer_delta[r] for r < n_peers (<= FO_MAX_PEERS) -- the same
+ * flat offset in each peer's parameter buffer, mapped into this process with
+ * fo_ipc_open -- so the all-gather of the bf16 weights happens inside the
+ * step, tile by tile, over NVLink.  One hyper-parameter set, the default
+ * layout (int8 corrections, companded variance, group size 32, 16-byte
+ * aligned views; FO_EUNSUPPORTED otherwise).  The caller orders the peers'
+ * next reads after every rank's step (a cross-rank barrier on the stream). */
+int fo_step_mt_peers(int optimizer, const fo_tensor *tensors, int32_t n_tensors, const fo_hparams *hparams,
+                     int grad_dtype, const int64_t *peer_delta, int32_t n_peers, uint32_t *d_err, void *stream);
+
+/* CUDA IPC for the peer mirrors.  fo_ipc_export: a 64-byte handle of the
+ * allocation holding `ptr` and ptr's byte offset in it.  fo_ipc_open (in
+ * another process): the mapped address of that byte; fo_ipc_close unmaps
+ * (pass the address and offset fo_ipc_open took). */
+int fo_ipc_export(const void *ptr, void *handle64, int64_t *offset);
+int fo_ipc_open(const void *handle64, int64_t offset, void **ptr);
+int fo_ipc_close(void *ptr, int64_t offset);
 
 /* Host table for fo_dev_scalars: out[4t .. 4t+3] = (bc1, RN(1/bc1), bc2,
  * RN(1/bc2)) of fo_make_hparams at step t, for t = 0 .. *len-1, where *len-1

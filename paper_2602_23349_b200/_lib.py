@@ -21,6 +21,7 @@ FO_OPT_SGD, FO_OPT_ADAMW, FO_OPT_LION = 0, 1, 2
 FO_GRAD_BF16, FO_GRAD_F32 = 0, 1
 FO_VAR_COMPANDED, FO_VAR_LINEAR = 0, 1
 FO_MAX_HPARAMS = 16
+FO_MAX_PEERS = 7
 OPT_TAGS = {"sgd": FO_OPT_SGD, "adamw": FO_OPT_ADAMW, "lion": FO_OPT_LION}
 
 ERR_GRAD_NONFINITE = 0x01
@@ -92,6 +93,11 @@ SIGNATURES = {
     "fo_step_mt_dev": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(fo_tensor), _I32, ctypes.POINTER(fo_hparams),
                                       ctypes.POINTER(fo_dev_scalars), ctypes.c_int, _P, _P]),
     "fo_bias_table": (ctypes.c_int, [_D, _D, _I32, _P, ctypes.POINTER(_I32)]),
+    "fo_step_mt_peers": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(fo_tensor), _I32, ctypes.POINTER(fo_hparams),
+                                        ctypes.c_int, ctypes.POINTER(_I64), _I32, _P, _P]),
+    "fo_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
+    "fo_ipc_open": (ctypes.c_int, [_P, _I64, ctypes.POINTER(ctypes.c_void_p)]),
+    "fo_ipc_close": (ctypes.c_int, [_P, _I64]),
 }
 
 _lib = None

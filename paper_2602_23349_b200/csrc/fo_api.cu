@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstring>
 
 #include "fo_internal.h"
 
@@ -131,6 +132,65 @@ int fo_step_mt_dev(int optimizer, const fo_tensor* tensors, int32_t n_tensors, c
                           dev->fix_count};
   return fo::step_mt(optimizer, tensors, n_tensors, &h, 1, grad_dtype, 8, 32, FO_VAR_COMPANDED, d_err,
                      as_stream(stream), &ds);
+}
+
+int fo_step_mt_peers(int optimizer, const fo_tensor* tensors, int32_t n_tensors, const fo_hparams* hparams,
+                     int grad_dtype, const int64_t* peer_delta, int32_t n_peers, uint32_t* d_err, void* stream) {
+  if (check_opt(optimizer) || n_tensors < 0 || (n_tensors && !tensors) || !hparams) return FO_EINVAL;
+  if (n_peers < 0 || n_peers > FO_MAX_PEERS || (n_peers && !peer_delta)) return FO_EINVAL;
+  if (grad_dtype != FO_GRAD_BF16 && grad_dtype != FO_GRAD_F32) return FO_EINVAL;
+  for (int32_t i = 0; i < n_tensors; ++i) {
+    const fo_tensor& t = tensors[i];
+    if (t.n < 0 || t.hp_index != 0) return FO_EINVAL;
+    if (t.n == 0) continue;
+    if (!t.lp || !t.rho || !t.m_codes || !t.m_scales || !t.grad) return FO_EINVAL;
+    if (optimizer == FO_OPT_ADAMW && (!t.v_codes || !t.v_scales)) return FO_EINVAL;
+  }
+  fo::DevScalars ds{};
+  ds.npeers = n_peers;
+  ds.peer_delta = peer_delta;
+  return fo::step_mt(optimizer, tensors, n_tensors, hparams, 1, grad_dtype, 8, 32, FO_VAR_COMPANDED, d_err,
+                     as_stream(stream), n_peers ? &ds : nullptr);
+}
+
+int fo_ipc_export(const void* ptr, void* handle64, int64_t* offset) {
+  if (!ptr || !handle64 || !offset) return FO_EINVAL;
+  // the allocation's base: cuMemGetAddressRange through the runtime's
+  // driver entry point (no libcuda link)
+  typedef int (*GetRange)(uintptr_t*, size_t*, uintptr_t);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return (int)cudaErrorNotSupported;
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  uintptr_t base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<uintptr_t>(ptr)) != 0) return (int)cudaErrorInvalidValue;
+  cudaIpcMemHandle_t h;
+  const cudaError_t rc = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (rc != cudaSuccess) return (int)rc;
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = (int64_t)(reinterpret_cast<uintptr_t>(ptr) - base);
+  return 0;
+}
+
+int fo_ipc_open(const void* handle64, int64_t offset, void** ptr) {
+  if (!handle64 || !ptr || offset < 0) return FO_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  void* base = nullptr;
+  const cudaError_t rc = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (rc != cudaSuccess) return (int)rc;
+  *ptr = static_cast<char*>(base) + offset;
+  return 0;
+}
+
+int fo_ipc_close(void* ptr, int64_t offset) {
+  if (!ptr || offset < 0) return FO_EINVAL;
+  return (int)cudaIpcCloseMemHandle(static_cast<char*>(ptr) - offset);
 }
 
 int fo_bias_table(double beta1, double beta2, int32_t max_len, float* out, int32_t* len) {

@@ -23,6 +23,9 @@ struct DevScalars {
   uint32_t* fix_bits;  // caller-owned fix-up bitmap (no allocation on the launch path)
   int64_t fix_words;
   unsigned long long* fix_count;
+  // fo_step_mt_peers: mirror every updated weights.lp to these byte deltas
+  int32_t npeers;
+  const int64_t* peer_delta;
 };
 int64_t fix_words_for(const fo_tensor* ts, int32_t nt);  // fo_step_adamw.cu
 

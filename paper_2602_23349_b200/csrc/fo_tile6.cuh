@@ -64,6 +64,19 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   return r;
 }
 
+// Peer mirrors of the bf16 weights (the fused step + all-gather): every
+// updated weights.lp value is also stored at its address + delta[r] (bytes)
+// for r < n -- the same flat offset in peer r's parameter buffer, mapped
+// into this process with CUDA IPC (zero.py, fused_allgather).
+struct PeerSet {
+  const int64_t* delta;
+  int n;
+  template <typename T>
+  __device__ __forceinline__ T* at(T* p, int r) const {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(p) + delta[r]);
+  }
+};
+
 // (~t & 0x7F800000) | 0x007E0000 as one LOP3 (left to itself ptxas emits a
 // mask and an XOR): K * 2^-13 of the split, see compute_tile6.
 __device__ __forceinline__ uint32_t k13_bits(uint32_t t) {
@@ -291,10 +304,11 @@ __device__ __forceinline__ float2 root2(float2 x) {
 // reference's error conditions (non-finite values, rho = -128, scale
 // overflow) remain; those go to process_tile_exact, which reports them.
 template <int OPT, typename GradT, int BC, class Src, class Lut, bool SAFE = false, int NCORR = 127,
-          bool LINEAR = false>
+          bool LINEAR = false, bool PEER = false>
 __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h, int64_t base, int lane,
                                               uint32_t& err, const Lut& L, float negzero, uint32_t* fix,
-                                              uint32_t fix_idx, bool full, const Src& in) {
+                                              uint32_t fix_idx, bool full, const Src& in,
+                                              const PeerSet& peers = PeerSet{nullptr, 0}) {
   using namespace fast;
   constexpr bool ADAM = (OPT == FO_OPT_ADAMW);
   constexpr int E = FEPL, NW = E / 2, NB = E / 4, LPG = GROUP / E;
@@ -628,7 +642,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
 
   // ---- any guard tripped anywhere in the warp: recompute the tile exactly ----
   if (__any_sync(0xffffffffu, bad)) {
-    if (SAFE) process_tile_exact<OPT, GradT, FEPL>(T, h, base, lane, fix);  // `fix` = error word here
+    if (SAFE) process_tile_exact<OPT, GradT, FEPL, 127, false, PEER>(T, h, base, lane, fix, &peers);  // `fix` = error word here
     else if (lane == 0) atomicOr(fix + (fix_idx >> 5), 1u << (fix_idx & 31));
     return;
   }
@@ -636,8 +650,12 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
   // ---- stores ----
   if (full) {
 #pragma unroll
-    for (int c = 0; c < NW / 4; ++c)
-      stcs4(T.lp + e0 + 8 * c, make_uint4(cw[4 * c], cw[4 * c + 1], cw[4 * c + 2], cw[4 * c + 3]));
+    for (int c = 0; c < NW / 4; ++c) {
+      const uint4 wv = make_uint4(cw[4 * c], cw[4 * c + 1], cw[4 * c + 2], cw[4 * c + 3]);
+      stcs4(T.lp + e0 + 8 * c, wv);
+      if (PEER)
+        for (int r = 0; r < peers.n; ++r) stcs4(peers.at(T.lp + e0 + 8 * c, r), wv);
+    }
     if (C16) {
       int16_t* r16 = reinterpret_cast<int16_t*>(T.rho) + e0;
       stcs4(r16, make_uint4(ro[0], ro[1], ro[2], ro[3]));
@@ -653,6 +671,8 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       const int64_t i = e0 + j;
       if (i < n) {
         T.lp[i] = (uint16_t)(cw[j >> 1] >> (16 * (j & 1)));
+        if (PEER)
+          for (int r = 0; r < peers.n; ++r) *peers.at(T.lp + i, r) = (uint16_t)(cw[j >> 1] >> (16 * (j & 1)));
         if (C16) reinterpret_cast<int16_t*>(T.rho)[i] = (int16_t)(ro[j >> 1] >> (16 * (j & 1)));
         else T.rho[i] = (int8_t)(ro[j >> 2] >> (8 * (j & 3)));
         T.mq[i] = (int8_t)(mo[j >> 2] >> (8 * (j & 3)));
@@ -697,9 +717,9 @@ __device__ __forceinline__ void load6_global_full(const TArg& T, int64_t base, i
 
 // One flagged slice in the fix-up launch: the SAFE tile (exact everywhere the
 // fast one needed guards), or the straight restatement for error cases.
-template <int OPT, typename GradT, int BC, int NCORR = 127, bool LINEAR = false>
+template <int OPT, typename GradT, int BC, int NCORR = 127, bool LINEAR = false, bool PEER = false>
 __device__ __forceinline__ void safe_tile(const TArg& T, const fo_hparams& h, int64_t base, int lane, float negzero,
-                                          uint32_t* err_out) {
+                                          uint32_t* err_out, const PeerSet& peers = PeerSet{nullptr, 0}) {
   if constexpr (NCORR != 127 || LINEAR) {
     // the optional layouts' flagged slices: the straight restatement
     (void)negzero;
@@ -713,6 +733,7 @@ __device__ __forceinline__ void safe_tile(const TArg& T, const fo_hparams& h, in
     const RegSrc<GradT> src{in, in.msb, in.vsb};
     uint32_t err = 0;
     const NoLut L;
-    compute_tile6<OPT, GradT, BC, RegSrc<GradT>, NoLut, true>(T, h, base, lane, err, L, negzero, err_out, 0, full, src);
+    compute_tile6<OPT, GradT, BC, RegSrc<GradT>, NoLut, true, 127, false, PEER>(T, h, base, lane, err, L, negzero,
+                                                                               err_out, 0, full, src, peers);
   }
 }

@@ -123,6 +123,20 @@ class StepPlan:
             self.table[i].grad = p
         self._grad_ptrs = ptrs
 
+    def launch_peers(self, hparams: _lib.fo_hparams, peer_delta, npeers: int, err_ptr: int | None,
+                     stream_handle: int) -> None:
+        """The fused step + all-gather (fo_step_mt_peers): every updated
+        weights.lp value is also written at the byte deltas `peer_delta`
+        (one hyper-parameter set; the default layout)."""
+        if self.rho_bits != 8 or self.group_size != 32 or self.var_scheme != _lib.FO_VAR_COMPANDED:
+            raise ValueError("the fused all-gather takes the default layout only")
+        hp = (_lib.fo_hparams * 1)(hparams)
+        _lib.check(_lib.lib().fo_step_mt_peers(self.tag, self.table, len(self.states), hp, self.grad_dtype,
+                                               peer_delta, npeers, err_ptr, stream_handle),
+                   "fo_step_mt_peers")
+        for st in self.states:
+            st.t += 1
+
     def launch(self, hparams: Sequence[_lib.fo_hparams], err_ptr: int | None, stream_handle: int) -> None:
         hp = (_lib.fo_hparams * len(hparams))(*hparams)
         _lib.check(_lib.lib().fo_step_mt(self.tag, self.table, len(self.states), hp, len(hparams),

@@ -17,6 +17,14 @@ because every operation is elementwise or reduces within one group
 (SURVEY Appendix B probe 6).  Only the owned pieces of the gradients are
 kept after the reduce-scatter.
 
+With `fused_allgather=True` there is no separate all-gather: every rank
+maps the other ranks' flat parameter buffers into its address space (CUDA
+IPC, fo_ipc_export / fo_ipc_open), and the fused step stores each updated
+bf16 weight both locally and at the same flat offset in every peer's buffer
+(fo_step_mt_peers), so the exchange of the new weights runs inside the step,
+tile by tile, over NVLink; a cross-rank barrier on the stream orders the
+peers' next reads.  One hyper-parameter set, the default layout.
+
 With `overlap_grad_reduce=True` a post-accumulate-grad hook counts the
 gradients that have arrived per bucket and launches that bucket's
 reduce-scatter asynchronously as soon as it is complete, so the exchange
@@ -119,7 +127,7 @@ class ZeroFlashOptimizer:
     def __init__(self, params: Sequence[torch.Tensor], optimizer: str, hparams: Sequence, group_of=None,
                  process_group=None, step_fn: Callable | None = None, reduce_op: str = "avg",
                  bucket_elems: int | None = None, overlap_grad_reduce: bool = False,
-                 check_errors: bool | str = "deferred"):
+                 check_errors: bool | str = "deferred", fused_allgather: bool = False):
         from .flat import FlatStates
 
         self.pg = process_group
@@ -190,6 +198,63 @@ class ZeroFlashOptimizer:
             for p in self.params:
                 self._hooks.append(p.register_post_accumulate_grad_hook(
                     lambda p, i=index[id(p)]: self._on_grad(i)))
+        self.fused_allgather = bool(fused_allgather)
+        self._peer_ptrs: list = []
+        self._peer_delta = None
+        if self.fused_allgather:
+            self._map_peers()
+
+    # -- peer memory (fused_allgather) -------------------------------------------------
+    def _map_peers(self) -> None:
+        """Exchange CUDA IPC handles of the flat parameter buffers and map every
+        peer's buffer: delta[r] = (peer r's buffer in this process) - (ours)."""
+        import ctypes
+
+        from . import _lib
+
+        if self.device.type != "cuda" or self.step_fn is not None:
+            raise ValueError("fused_allgather needs the CUDA step")
+        if len(self.hparams) != 1:
+            raise ValueError("fused_allgather takes one hyper-parameter set")
+        if self.world - 1 > _lib.FO_MAX_PEERS:
+            raise ValueError(f"fused_allgather maps at most {_lib.FO_MAX_PEERS} peers")
+        L = _lib.lib()
+        handle = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64(0)
+        _lib.check(L.fo_ipc_export(self.flat_params.data_ptr(), handle, ctypes.byref(off)), "fo_ipc_export")
+        mine = (bytes(handle.raw), int(off.value))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=self.pg)
+        deltas = []
+        for r, (h, o) in enumerate(allh):
+            if r == self.rank:
+                continue
+            buf = ctypes.create_string_buffer(h, 64)
+            ptr = ctypes.c_void_p(0)
+            _lib.check(L.fo_ipc_open(buf, o, ctypes.byref(ptr)), "fo_ipc_open")
+            self._peer_ptrs.append((int(ptr.value), o))
+            deltas.append(int(ptr.value) - self.flat_params.data_ptr())
+        self._peer_delta = (ctypes.c_int64 * max(1, len(deltas)))(*deltas)
+        self._npeers = len(deltas)
+
+    def close(self) -> None:
+        """Unmap the peers' parameter buffers (fused_allgather)."""
+        from . import _lib
+
+        torch.cuda.synchronize(self.device)
+        for ptr, o in self._peer_ptrs:
+            _lib.lib().fo_ipc_close(ptr, o)
+        self._peer_ptrs = []
+
+    def _peer_barrier(self) -> None:
+        """Every rank's fused step (and its stores into our buffer) before our
+        next read of the parameters."""
+        if self._staged():
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.pg)
+        else:  # on the stream: completes only once every rank's step has finished
+            t = torch.zeros(1, dtype=torch.int32, device=self.device)
+            dist.all_reduce(t, group=self.pg)
 
     # -- collectives (host-staged for gloo with CUDA tensors) -----------------------
     def _staged(self) -> bool:
@@ -287,7 +352,11 @@ class ZeroFlashOptimizer:
         if self._plan is None:
             self._plan = StepPlan(self.optimizer, self.states, [s.hp_index for s in self.segments])
             self._plan.set_grads(grads)
-        self._plan.launch(self._scalars(), self._errors.ptr, stream_handle(self.device))
+        if self.fused_allgather:
+            self._plan.launch_peers(self._scalars()[0], self._peer_delta, self._npeers, self._errors.ptr,
+                                    stream_handle(self.device))
+        else:
+            self._plan.launch(self._scalars(), self._errors.ptr, stream_handle(self.device))
 
     def all_gather_params(self) -> None:
         works = []
@@ -304,7 +373,10 @@ class ZeroFlashOptimizer:
     def step(self) -> None:
         self.reduce_scatter_grads()
         self.step_shard()
-        self.all_gather_params()
+        if self.fused_allgather:
+            self._peer_barrier()
+        else:
+            self.all_gather_params()
         self.t += 1
         if self._errors is not None:
             self._errors.after_step(self.optimizer)

@@ -5,7 +5,12 @@ steps every rank's full bf16 parameters and every owned segment's state must
 equal an unsharded oracle run bit for bit.  Gradients are exact under the
 reduction: rank 0's backward yields g, rank 1's exactly zero.
 Covers bucketed ownership, the reduce-scatter started from backward hooks,
-fp32 parameters split at construction, and the batched rank-0 checkpoint."""
+fp32 parameters split at construction, and the batched rank-0 checkpoint.
+With fused_allgather=True there is no all-gather: each rank's fused step
+stores its updated weights into the other rank's parameter buffer through
+CUDA IPC (two processes on one device exercise the same peer-store path
+as two GPUs over NVLink), and every rank's parameters must still equal the
+oracle's after every step."""
 
 from __future__ import annotations
 
@@ -19,7 +24,8 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-SIZES = [1000, 4096 + 7, 33, 70_000, 1, 40_960]
+SIZES = [1000, 4096 + 7, 33, 70_000, 1, 40_960, 8192]
+ZERO = 6  # an all-zero tensor with zero gradients: its slices trip the fast tile's guards (fix-up path)
 STEPS = 3
 HP = {"adamw": dict(lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1),
       "sgd": dict(lr=0.1, momentum=0.9, weight_decay=1e-4),
@@ -36,15 +42,19 @@ def _free_port() -> int:
 
 def _theta0():
     g = torch.Generator().manual_seed(11)
-    return [(torch.randn(n, generator=g) * 0.02) for n in SIZES]  # fp32 master weights
+    t = [(torch.randn(n, generator=g) * 0.02) for n in SIZES]  # fp32 master weights
+    t[ZERO].zero_()
+    return t
 
 
 def _grads(step):
     g = torch.Generator().manual_seed(500 + step)
-    return [(torch.randn(n, generator=g) * 1e-3).to(torch.bfloat16) for n in SIZES]
+    gs = [(torch.randn(n, generator=g) * 1e-3).to(torch.bfloat16) for n in SIZES]
+    gs[ZERO].zero_()
+    return gs
 
 
-def _worker(rank, world, port, opt, q, directory):
+def _worker(rank, world, port, opt, q, directory, fused=False):
     try:
         import sys
 
@@ -61,7 +71,7 @@ def _worker(rank, world, port, opt, q, directory):
 
         params = [t.cuda().requires_grad_() for t in _theta0()]
         zo = ZeroFlashOptimizer(params, opt, [FO.HP_TYPES[opt](**HP[opt])], reduce_op="sum", bucket_elems=8192,
-                                overlap_grad_reduce=True, check_errors=True)
+                                overlap_grad_reduce=True, check_errors=True, fused_allgather=fused)
         for s in range(STEPS):
             zo.zero_grad()
             gs = [g.cuda() for g in _grads(s)]
@@ -78,8 +88,13 @@ def _worker(rank, world, port, opt, q, directory):
                   "v": None if st.variance is None else st.variance.codes.cpu().numpy(),
                   "vs": None if st.variance is None else st.variance.scales.cpu().numpy()})
                 for seg, st in zip(zo.segments, zo.states)]
-        q.put((rank, full, segs))
+        from paper_2602_23349_b200 import _lib
+
+        flagged, _ = _lib.fixup_stats()
+        q.put((rank, full, segs, flagged))
         dist.barrier()
+        if fused:
+            zo.close()
         dist.destroy_process_group()
     except BaseException:
         import traceback
@@ -88,8 +103,9 @@ def _worker(rank, world, port, opt, q, directory):
         raise
 
 
+@pytest.mark.parametrize("fused", [False, True], ids=["nccl_allgather", "fused_allgather"])
 @pytest.mark.parametrize("opt", ["adamw", "sgd", "lion"])
-def test_zero1_two_ranks_cuda_step(opt, cuda_dev, oracle_mod, tmp_path):
+def test_zero1_two_ranks_cuda_step(opt, fused, cuda_dev, oracle_mod, tmp_path):
     from paper_2602_23349_b200.checkpoint import save_checkpoint
     from paper_2602_23349_b200.host import HostFlashState
 
@@ -97,7 +113,7 @@ def test_zero1_two_ranks_cuda_step(opt, cuda_dev, oracle_mod, tmp_path):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, opt, q, d)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, opt, q, d, fused)) for r in range(2)]
     for p in procs:
         p.start()
     got = [q.get(timeout=600) for _ in range(2)]
@@ -105,7 +121,8 @@ def test_zero1_two_ranks_cuda_step(opt, cuda_dev, oracle_mod, tmp_path):
         p.join(timeout=120)
     errs = [x[2] for x in got if isinstance(x[1], str)]
     assert not errs, errs[0]
-    res = {r: (f, s) for r, f, s in got}
+    res = {r: (f, s) for r, f, s, _ in got}
+    assert sum(x[3] for x in got) > 0  # the fix-up launch re-ran (and mirrored) flagged slices
     states = [oracle_mod.init_state(t.numpy(), opt) for t in _theta0()]
     for s in range(STEPS):
         for st, g in zip(states, _grads(s)):
