@@ -813,6 +813,26 @@ def run_ours(args) -> None:
     launches_per_step = 2 * ((len(states) + 383) // 384)  # fused step + fix-up per <= 384 tensors
     traffic, traffic_src = traffic_for(args, n_local)
 
+    # One more launch after the board has idled for a second: the same kernel
+    # before the 1000 W power limit pulls the clock down (informational; the
+    # headline is the back-to-back average above).
+    single = None
+    if world == 1 and zo is None:
+        import time as _time
+
+        torch.cuda.synchronize()
+        _time.sleep(1.0)
+        a1, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a1.record(stream)
+        one_step()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        ms1 = a1.elapsed_time(b1)
+        single = {"ms": ms1, "gparams_s": n_all / (ms1 * 1e-3) / 1e9,
+                  "frac_of_peak": n_local * bpp / (ms1 * 1e-3) / 1e9 / peak,
+                  "note": "one launch after 1 s idle (clock not yet pulled down by the power limit); "
+                          "not the headline"}
+
     zero1 = None
     if zo is not None:
         zero1 = zero1_phases(zo, args, dev, stream, reduce_, n_all)
@@ -862,7 +882,7 @@ def run_ours(args) -> None:
                           "share": (1.0 - flagged / slices) if slices else None,
                           "note": "512-element slices stored by the fused tile vs re-run by the fix-up launch "
                                   "(fo_fixup_stats, timed region)"},
-            "parity": parity, "e2e": e2e, "cpu_baseline": cpu, "zero1": zero1,
+            "parity": parity, "e2e": e2e, "cpu_baseline": cpu, "zero1": zero1, "single_launch_after_idle": single,
             "clocks": clk, "power": pwr, "gpu_launches": args.steps * launches_per_step,
             "device_errors": emask,
         }
