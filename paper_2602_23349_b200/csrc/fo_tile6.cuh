@@ -34,6 +34,17 @@
 #endif
 // Split code from a K * 2^-13 made by one LOP3 (1 instead of 2 integer ops
 // per element); 0: K = 127 * 2^-ell by LOP3 + IADD3.
+// FO_MQ_APPROX=1: momentum codes from an approximate quotient with an
+// exactness check on the rounding distance (exact fallback per lane).
+#ifndef FO_MQ_APPROX
+#define FO_MQ_APPROX 1
+#endif
+// FO_PROBE (energy measurements only, results NOT exact): 1 momentum
+// quotients -> one multiply, 2 variance quotient -> one multiply, 3 the
+// update's division -> a multiply.
+#ifndef FO_PROBE
+#define FO_PROBE 0
+#endif
 #ifndef FO_SPLIT_K13
 #define FO_SPLIT_K13 1
 #endif
@@ -493,7 +504,11 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       // the quantity the variance epilogue groups: the root (companded) or v (linear)
       root[j] = LINEAR ? v2.x : rt2.x;
       root[j + 1] = LINEAR ? v2.y : rt2.y;
+#if FO_PROBE == 3  // energy probe (not exact): no division in the update
+      const float2 u = add2(mul2(mh, den), fma2(dup(h.wd), th2, Z));
+#else
       const float2 u = add2(quot<SAFE>(mh, den), fma2(dup(h.wd), th2, Z));
+#endif
       tn2 = add2(th2, neg2(fma2(dup(h.lr), u, Z)));
     } else if (OPT == FO_OPT_SGD) {
       m2 = add2(fma2(dup(h.mu), mp2, Z), g2);
@@ -601,17 +616,59 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const float s = half_bits_to_float(new_msb);
     const float den = (s == 0.0f) ? 1.0f : s;
     const float y = rcp_rn_normal(den);
+#if FO_MQ_APPROX
+    if (!SAFE) {
+      // T = 254 m' / (1 + |m'|) without the two exact quotients: m' ~ m *
+      // RN(254 / s), 1 + |m'| by one FFMA, one MUFU reciprocal.  |T - T_ref|
+      // < 2^-12 against the reference's RN(RN(RN(m/s) / RN(1 + |m/s|)) * 254)
+      // (error budget in DESIGN.md §3.2; selftest modes 8-9), so wherever T
+      // is at least 2^-12 away from a half-integer rint(T) is the reference's
+      // code.  A lane with any element closer than that recomputes its codes
+      // exactly below (one element in ~2000).
+      const float y254 = __fmul_rn(y, 254.0f);
+      float emax = 0.0f;
+#pragma unroll
+      for (int j = 0; j < E; j += 2) {
+        const float2 T = mq_T(make_float2(m[j], m[j + 1]), y254);
+        const float2 t = add2(T, dup(12582912.0f));  // rint(T) in the low bits
+        const float2 e = add2(T, neg2(add2(t, dup(-12582912.0f))));  // T - rint(T)
+        emax = fmaxf(emax, fmaxf(fabsf(e.x), fabsf(e.y)));
+        const uint32_t pr = prmt(__float_as_uint(t.x), __float_as_uint(t.y), 0x0040u);
+        if (j & 2) mo[j >> 2] = prmt(mo[j >> 2], pr, 0x5410u);
+        else mo[j >> 2] = pr;
+      }
+      if (!(emax <= 0.5f - 0x1p-12f)) {
+#pragma unroll
+        for (int j = 0; j < E; j += 2) {
+          const float2 mn = quot_y<SAFE>(make_float2(m[j], m[j + 1]), den, y);
+          const float2 d = make_float2(__fadd_rn(1.0f, fabsf(mn.x)), __fadd_rn(1.0f, fabsf(mn.y)));
+          const float2 zh = quot<SAFE>(mn, d);
+          const float2 t = add2(fma2(zh, dup(254.0f), Z), dup(12582912.0f));
+          const uint32_t pr = prmt(__float_as_uint(t.x), __float_as_uint(t.y), 0x0040u);
+          if (j & 2) mo[j >> 2] = prmt(mo[j >> 2], pr, 0x5410u);
+          else mo[j >> 2] = pr;
+        }
+      }
+    } else {
+#else
+    {
+#endif
 #pragma unroll
     for (int j = 0; j < E; j += 2) {
+#if FO_PROBE == 1  // energy probe (not exact): momentum codes by one multiply
+      const float2 zh = mul2(make_float2(m[j], m[j + 1]), dup(y));
+#else
       const float2 mn = quot_y<SAFE>(make_float2(m[j], m[j + 1]), den, y);  // RN(m/s)
       const float2 d = make_float2(__fadd_rn(1.0f, fabsf(mn.x)), __fadd_rn(1.0f, fabsf(mn.y)));
       // RN(2m'/(1+|m'|)) = 2*RN(m'/(1+|m'|)) (power-of-two scaling), so
       // RN(z*127) = RN(RN(m'/d)*254)
       const float2 zh = quot<SAFE>(mn, d);
+#endif
       const float2 t = add2(fma2(zh, dup(254.0f), Z), dup(12582912.0f));  // rint(RN(z*127))
       const uint32_t pr = prmt(__float_as_uint(t.x), __float_as_uint(t.y), 0x0040u);
       if (j & 2) mo[j >> 2] = prmt(mo[j >> 2], pr, 0x5410u);
       else mo[j >> 2] = pr;
+    }
     }
   }
 
@@ -632,7 +689,11 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     const float y = QSCALED ? __fmul_rn(rcp_rn_normal((s == 0.0f) ? 1.0f : s), 1.0f / RS) : rcp_rn_normal(den);
 #pragma unroll
     for (int j = 0; j < E; j += 2) {
+#if FO_PROBE == 2  // energy probe (not exact): variance codes by one multiply
+      const float2 vn = mul2(make_float2(root[j], root[j + 1]), dup(y));
+#else
       const float2 vn = quot_y<SAFE>(make_float2(root[j], root[j + 1]), den, y);  // RN(r/s)
+#endif
       const float2 t = add2(fma2(vn, dup(255.0f), Z), dup(12582912.0f));           // rint(RN(vn*255))
       const uint32_t pr = prmt(__float_as_uint(t.x), __float_as_uint(t.y), 0x0040u);
       if (j & 2) vo[j >> 2] = prmt(vo[j >> 2], pr, 0x5410u);

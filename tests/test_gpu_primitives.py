@@ -68,3 +68,18 @@ def test_integer_reconstruct_exhaustive(cuda_dev):
     the two zero cases it gets wrong come out NaN or -0 (guard-tripping)."""
     bad, first = _run(6, 0, 1 << 24)
     assert bad == 0, f"{bad} mismatches, first at code {first >> 8:#06x} rho byte {first & 0xFF:#04x}"
+
+
+def test_rcp_approx_error_bound(cuda_dev):
+    """MUFU reciprocal: relative error < 2^-22 for every f32 in [1, 2) (the
+    bound the approximate momentum coder's error budget uses)."""
+    bad, first = _run(8, 0, 1 << 23)
+    assert bad == 0, f"{bad} inputs over the bound, first mantissa {first:#x}"
+
+
+def test_momentum_preimage_bound_sampled(cuda_dev):
+    """mq_T (FO_MQ_APPROX) within 2^-12 of the reference's pre-rint momentum
+    value, and its rint equal to the reference code away from half-integers:
+    2^32 samples over every fp16 scale (quantize.py:109-122)."""
+    bad, first = _run(9, 0, 1 << 32)
+    assert bad == 0, f"{bad} violations, first sample {first}"
