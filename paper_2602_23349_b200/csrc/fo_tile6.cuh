@@ -41,7 +41,7 @@
 #endif
 // FO_PROBE (energy measurements only, results NOT exact): 1 momentum
 // quotients -> one multiply, 2 variance quotient -> one multiply, 3 the
-// update's division -> a multiply.
+// update's division -> a multiply, 4 no range guards, 5 no moment LUT lookups.
 #ifndef FO_PROBE
 #define FO_PROBE 0
 #endif
@@ -421,7 +421,7 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
         for (int q = 0; q < 4; ++q) rmin = __vmins2(rmin, hr[q]);
       } else {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) rmin = __vmins2(rmin, __vmins2(hr[q], hr[q] << 8));
+        for (int q = 0; q < 2; ++q) if (FO_PROBE != 4) rmin = __vmins2(rmin, __vmins2(hr[q], hr[q] << 8));
       }
     }
     const uint32_t w = hl[k & 3];
@@ -462,7 +462,12 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
       th2 = make_float2(__uint_as_float(recon_bits(w << 16, rl)), __uint_as_float(recon_bits(w & 0xFFFF0000u, rh)));
     }
     // dequantise (quantize.py:125-131, :152-158)
+#if FO_PROBE == 5  // energy probe (not exact): no moment LUT lookups
+    const float2 u2 = make_float2(__uint_as_float(0x3F000000u | ((mwd >> (8 * (j & 3))) & 0xFFu)),
+                                  __uint_as_float(0x3F000000u | (mwd & 0xFF00u)));
+#else
     const float2 u2 = make_float2(L.m(mwd, j & 3), L.m(mwd, (j & 3) + 1));
+#endif
     const float2 mp2 = fma2(u2, dup(msf), Z);
     float2 g2;
     if (sizeof(GradT) == 2) {
@@ -474,14 +479,19 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     // update (optim.py:195-198, :220-226, :247-249)
     float2 m2, tn2;
     if (OPT == FO_OPT_ADAMW) {
+#if FO_PROBE == 5
+      const float2 z2 = make_float2(__uint_as_float(0x3F000000u | ((vwd >> (8 * (j & 3))) & 0xFFu)),
+                                    __uint_as_float(0x3F000000u | (vwd & 0xFF00u)));
+#else
       const float2 z2 = make_float2(L.v(vwd, j & 3), L.v(vwd, (j & 3) + 1));
+#endif
       const float2 r2 = fma2(z2, dup(vsf), Z);              // quantize.py:157 (linear: v itself, :185)
       const float2 vp2 = LINEAR ? r2 : fma2(r2, r2, Z);
       m2 = add2(fma2(dup(h.b1), mp2, Z), fma2(dup(h.omb1), g2, Z));
       const float2 v2 = add2(fma2(dup(h.b2), vp2, Z), fma2(dup(h.omb2), fma2(g2, g2, Z), Z));
       constexpr bool WIDE_ROOT = FO_SQRT_WIDE && (BC & 2) && !SAFE;
       if (!SAFE && VG) {
-        mlo = __vimin3_u32(mlo, (__float_as_uint(m2.x) << 1) - 2u, (__float_as_uint(m2.y) << 1) - 2u);
+        if (FO_PROBE != 4) mlo = __vimin3_u32(mlo, (__float_as_uint(m2.x) << 1) - 2u, (__float_as_uint(m2.y) << 1) - 2u);
         if (!WIDE_ROOT) vlo = __vimin3_u32(vlo, (__float_as_uint(v2.x) << 1) - 2u, (__float_as_uint(v2.y) << 1) - 2u);
       }
       const float2 mh = (BC & 1) ? m2 : quot_y<SAFE>(m2, h.bc1, h.rbc1);
@@ -580,8 +590,10 @@ __device__ __forceinline__ void compute_tile6(const TArg& T, const fo_hparams& h
     if (C16) ro[k] = pr;
     else if (k & 1) ro[k >> 1] = prmt(ro[k >> 1], pr, 0x5410u);
     else ro[k >> 1] = pr;
-    tmin = fminf(tmin, fminf(fabsf(tn2.x), fabsf(tn2.y)));
-    tmax = maxnan3(tmax, fabsf(tn2.x), fabsf(tn2.y));
+    if (FO_PROBE != 4) {
+      tmin = fminf(tmin, fminf(fabsf(tn2.x), fabsf(tn2.y)));
+      tmax = maxnan3(tmax, fabsf(tn2.x), fabsf(tn2.y));
+    }
   }
   // |theta_new| in [2^-113, bf16 max): the split's exponent rule holds, and
   // the reconstruct's zero cases (NaN, or a zero whose sign may differ from
