@@ -195,6 +195,35 @@ __device__ __forceinline__ void load6_global(const TArg& T, int64_t base, int la
   constexpr int E = FEPL, NW = E / 2, NB = E / 4, NG = TileIn6<GradT, NCORR>::NG, NR = TileIn6<GradT, NCORR>::NR;
   const int64_t n = T.n;
   const int64_t e0 = base + (int64_t)lane * E;
+  if (e0 + E <= n) {
+    // a lane whose 16 elements are all inside the tensor: 128-bit loads (the
+    // fused paths take 16-byte aligned views only, and e0 is a multiple of 16)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const uint4 a = ldcs4(T.lp + e0 + 8 * c);
+      in.lw[4 * c] = a.x; in.lw[4 * c + 1] = a.y; in.lw[4 * c + 2] = a.z; in.lw[4 * c + 3] = a.w;
+    }
+#pragma unroll
+    for (int c = 0; c < NG / 4; ++c) {
+      const uint4 a = ldcs4(reinterpret_cast<const GradT*>(T.g) + e0 + (16 / sizeof(GradT)) * c);
+      in.gw[4 * c] = a.x; in.gw[4 * c + 1] = a.y; in.gw[4 * c + 2] = a.z; in.gw[4 * c + 3] = a.w;
+    }
+    if (NCORR == 127) {
+      load_bytes<4>(T.rho + e0, in.rw);
+    } else {
+      load_bytes<4>(reinterpret_cast<const int16_t*>(T.rho) + e0, in.rw);
+      load_bytes<4>(reinterpret_cast<const int16_t*>(T.rho) + e0 + 8, in.rw + 4);
+    }
+    load_bytes<4>(T.mq + e0, in.mw);
+    if (ADAM) load_bytes<4>(T.vq + e0, in.vw);
+    else {
+#pragma unroll
+      for (int q = 0; q < NB; ++q) in.vw[q] = 0;
+    }
+    in.msb = T.ms[e0 >> 5];
+    in.vsb = ADAM ? (uint32_t)T.vs[e0 >> 5] : 0u;
+    return;
+  }
   // elements past n: weight 1.0 (0x3F80), zero correction, codes, scales
   // and gradient -- their m and v are 0 (no effect on a group maximum) and
   // their updated weight stays near 1, so they trip no guard; they are

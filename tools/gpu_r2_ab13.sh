@@ -1,0 +1,7 @@
+for rep in 1 2; do for v in pv base; do FO_LIB_PATH=$PWD/build/$v/lib.so timeout 600 python tools/graph_step.py --steps 300 > gpurun_out/ab13_graph_$v.jsonl 2>/dev/null; python3 -c "
+import json
+for l in open('gpurun_out/ab13_graph_$v.jsonl'):
+    d=json.loads(l)
+    if d['mode']=='launch': print('$v', d['config'],d['optimizer'],'ms',round(d['ms'],4))
+"; done; done
+VARIANTS="pv:build/pv/lib.so: base:build/base/lib.so:" STEPS=150 REPS=3 bash tools/gpu_ab_power.sh 2>&1 | tail -6
