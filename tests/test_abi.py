@@ -177,3 +177,25 @@ def test_capturable_entry_points_validate_synchronously():
     assert L.fo_step_mt_dev(1, None, 0, ctypes.byref(hp), ctypes.byref(ds), 0, None, None) == -1  # adamw: no table
     ds.bc_table, ds.bc_len = 16, 40
     assert L.fo_step_mt_dev(1, None, 0, ctypes.byref(hp), ctypes.byref(ds), 0, None, None) == -1  # no bitmap
+
+
+def test_peer_entry_points_validate_synchronously():
+    """fo_step_mt_peers / fo_ipc_* reject bad arguments before any CUDA call."""
+    from paper_2602_23349_b200 import _lib
+
+    L = _lib.lib()
+    hp = _lib.make_hparams("adamw", 1e-3)
+    deltas = (ctypes.c_int64 * 8)()
+    assert L.fo_step_mt_peers(1, None, 0, ctypes.byref(hp), 0, deltas, 8, None, None) == -1  # > FO_MAX_PEERS
+    assert L.fo_step_mt_peers(1, None, 0, ctypes.byref(hp), 0, None, 2, None, None) == -1    # no deltas
+    assert L.fo_step_mt_peers(7, None, 0, ctypes.byref(hp), 0, deltas, 1, None, None) == -1  # optimizer
+    t = _lib.fo_tensor()
+    t.n, t.hp_index = 10, 1
+    assert L.fo_step_mt_peers(1, ctypes.byref(t), 1, ctypes.byref(hp), 0, deltas, 1, None, None) == -1
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    assert L.fo_ipc_export(None, h, ctypes.byref(off)) == -1
+    ptr = ctypes.c_void_p(0)
+    assert L.fo_ipc_open(None, 0, ctypes.byref(ptr)) == -1
+    assert L.fo_ipc_open(h, -1, ctypes.byref(ptr)) == -1
+    assert L.fo_ipc_close(None, 0) == -1
